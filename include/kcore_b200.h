@@ -1,0 +1,161 @@
+/*
+ * kcore_b200.h — C-ABI of the B200 (sm_100a) FastK coreness path.
+ *
+ * Drop-in boundary for the reference entry point
+ *     kcore::EngineResult kcore::fastk_run(const Graph&, const FastKOptions&,
+ *                                          const Instrumentation*)
+ * declared at /root/reference/proj/include/kcore/fastk.hpp:46-47 and defined at
+ * src/fastk.cpp:57-187.  Undirected CSR in (the reference Graph's
+ * offsets()/neighbors(), include/kcore/graph.hpp:53-59,72-73), per-vertex
+ * coreness out (CorenessResult::coreness, include/kcore/oracle.hpp:10-14),
+ * RunReport counters (include/kcore/report.hpp:17-23) in kc_stats.
+ *
+ * Plain C types only; no exceptions cross this boundary.  Every call is
+ * synchronous with respect to the host.  A kc_graph handle owns one CUDA
+ * stream and its device buffers; it is not thread-safe, distinct handles are.
+ * There is no CPU fallback: without a usable sm_100 device every entry point
+ * that needs one returns KC_ERR_NO_DEVICE.
+ */
+#ifndef KCORE_B200_H
+#define KCORE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KC_ABI_VERSION 1
+
+typedef enum kc_status {
+  KC_OK = 0,
+  KC_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument (fastk.cpp:58-59) */
+  KC_ERR_NO_DEVICE = 2,        /* no CUDA device / not sm_100 */
+  KC_ERR_OUT_OF_MEMORY = 3,    /* reference: std::bad_alloc */
+  KC_ERR_CUDA = 4,             /* any other CUDA runtime error */
+  KC_ERR_NOT_CONVERGED = 5,    /* round cap exceeded (never expected) */
+  KC_ERR_CALLBACK = 6          /* an inspector callback asked to stop */
+} kc_status;
+
+/* Activation rule.  Every rule reaches the same unique fixed
+ * point; they differ in how many vertices are re-evaluated per round. */
+typedef enum kc_rule {
+  /* extended_notify judged on SETTLED estimates after the round's updates —
+   * exactly fastk_run's notify phase (fastk.cpp:156-163).  With
+   * hybrid_tail = 0 the RunReport counters equal the reference's. */
+  KC_RULE_REFERENCE = 0,
+  /* every dropper re-activates itself, neighbours judged with the extended
+   * rule on the round's snapshot, in the same pass (no settled re-scan). */
+  KC_RULE_SNAPSHOT = 1,
+  KC_RULE_AUTO = 2 /* the fastest safe rule (currently KC_RULE_SNAPSHOT) */
+} kc_rule;
+
+/* FastKOptions (include/kcore/fastk.hpp:12-22) plus GPU knobs. */
+typedef struct kc_options {
+  uint32_t threads;        /* validated >= 1 like the reference; advisory on GPU */
+  uint32_t batch;          /* validated >= 1; hybrid switch threshold (fastk.hpp:29-31) */
+  int32_t extended_notify; /* fastk.hpp:18 */
+  int32_t hybrid_tail;     /* fastk.hpp:21: small-frontier single-CTA rounds */
+  int32_t rule;            /* kc_rule */
+  uint32_t max_rounds;     /* 0 = default safety cap */
+  uint32_t smem_cache;     /* ids whose estimates are cached in shared memory per
+                              round; 0 = default, 0xffffffff = disabled */
+  uint32_t reserved[8];
+} kc_options;
+
+/* RunReport (report.hpp:17-23) + work counters and timings. */
+typedef struct kc_stats {
+  uint64_t iterations;       /* executed rounds incl. the final quiescent one */
+  uint64_t messages_sent;    /* notifications fired */
+  uint64_t messages_drained; /* vertex evaluations (incl. isolated vertices in round 0) */
+  uint64_t tail_pops;        /* evaluations done in the single-CTA tail mode */
+  uint64_t e_scan;           /* adjacency entries scanned by evaluations */
+  uint64_t v_eval;           /* evaluations of non-isolated vertices */
+  uint64_t drops;            /* estimate decreases */
+  uint64_t tail_rounds;      /* rounds run in the single-CTA tail mode */
+  uint32_t k_max;            /* CorenessResult::k_max (oracle.hpp:12) */
+  uint32_t h_graph;          /* h-index of the degree sequence */
+  double k_avg;              /* CorenessResult::k_avg (oracle.hpp:13) */
+  float t_upload_ms;         /* H2D of the CSR (kc_graph_upload) */
+  float t_prep_ms;           /* on-device relabel / layout (kc_graph_upload) */
+  float t_solve_ms;          /* init -> converged estimates, CSR resident */
+  float t_download_ms;       /* permute-back + D2H of the coreness */
+  uint32_t reserved[8];
+} kc_stats;
+
+/* A borrowed view of an undirected simple CSR: offsets has n+1 entries,
+ * neighbors has offsets[n] entries, each row strictly increasing, mirrored
+ * (graph.hpp:31-36).  offsets/neighbors are HOST pointers unless stated. */
+typedef struct kc_csr_view {
+  uint32_t n;
+  uint64_t nnz;
+  const uint64_t* offsets;
+  const uint32_t* neighbors;
+} kc_csr_view;
+
+typedef struct kc_graph kc_graph;
+
+/* Per-round observation hook (report.hpp:33-39): called at iteration 0
+ * (degrees) and after every executed round, with the estimates in the
+ * caller's vertex ids.  Return non-zero to abort (KC_ERR_CALLBACK). */
+typedef int (*kc_inspector_fn)(void* user, uint64_t iteration, const uint32_t* estimates,
+                               uint32_t n, uint64_t active_count);
+
+const char* kc_status_str(kc_status s);
+int kc_abi_version(void);
+void kc_default_options(kc_options* opt);
+/* Last CUDA / validation error message of this thread ("" if none). */
+const char* kc_last_error(void);
+
+/* Upload a host CSR to `device` and lay it out for the solver (degree-sorted
+ * relabel, 32-bit offsets when nnz < 2^32).  Validates the view shape. */
+kc_status kc_graph_upload(const kc_csr_view* csr, int device, kc_graph** out);
+/* Same, but `csr` points at DEVICE memory on `device` (e.g. a graph built by
+ * kc_gen_*); the source buffers are only read. */
+kc_status kc_graph_upload_device(const kc_csr_view* csr, int device, kc_graph** out);
+void kc_graph_free(kc_graph* g);
+uint32_t kc_graph_n(const kc_graph* g);
+uint64_t kc_graph_nnz(const kc_graph* g);
+/* The upload / prep timings of the handle (ms). */
+kc_status kc_graph_timings(const kc_graph* g, float* t_upload_ms, float* t_prep_ms);
+
+/* Converge on the device; write coreness[n] (caller's ids) to HOST memory. */
+kc_status kc_solve(kc_graph* g, const kc_options* opt, uint32_t* coreness, kc_stats* stats);
+/* Same, coreness written to DEVICE memory (no D2H; CSR and result resident). */
+kc_status kc_solve_device(kc_graph* g, const kc_options* opt, uint32_t* coreness_dev,
+                          kc_stats* stats);
+/* Instrumented run: one round per launch, estimates copied out after each. */
+kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn fn,
+                            void* user, uint32_t* coreness, kc_stats* stats);
+
+/* One-shot drop-in: upload + solve + download + free (fastk_run semantics). */
+kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* coreness,
+                       kc_stats* stats);
+
+/* The CUDA stream a handle runs on (cudaStream_t as void*), for callers that
+ * want to time kc_solve_device with their own events. */
+void* kc_graph_stream(kc_graph* g);
+
+/* ---- synthetic inputs (BASELINE.json configs; the "kcgen v1" spec) ------ */
+/* Build one of the five configs (1..5) — or a scaled variant — directly on
+ * the device: CSR with uint64 offsets and uint32 neighbours in DEVICE memory
+ * owned by the returned kc_csr_dev (free with kc_csr_dev_free).
+ *   cfg 1: ER G(n, m)          p0 = n,     p1 = m
+ *   cfg 2: grid side x side    p0 = side
+ *   cfg 3/5: R-MAT             p0 = scale, p1 = edge factor
+ *   cfg 4: Chung-Lu            p0 = n,     p1 = cliques, p2 = clique size */
+typedef struct kc_csr_dev {
+  kc_csr_view view; /* device pointers */
+  int device;
+} kc_csr_dev;
+kc_status kc_gen_config(int cfg, uint64_t p0, uint64_t p1, uint64_t p2, uint64_t seed,
+                        int device, kc_csr_dev** out);
+void kc_csr_dev_free(kc_csr_dev* g);
+/* Copy a device CSR to host buffers (offsets n+1, neighbours nnz). */
+kc_status kc_csr_dev_download(const kc_csr_dev* g, uint64_t* offsets, uint32_t* neighbors);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KCORE_B200_H */

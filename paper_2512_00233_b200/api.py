@@ -1,0 +1,454 @@
+"""ctypes binding of include/kcore_b200.h and the reference-shaped Python API.
+
+Names, argument meaning and error behaviour mirror the reference C++ API
+(/root/reference/proj/include/kcore/*.hpp) so tests read like the
+reference's own (tests/test_fastk.cpp, tests/test_oracle.cpp).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Callable, Iterable, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libkcore_b200.so")
+
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+
+
+# --------------------------------------------------------------------------
+# C structs (include/kcore_b200.h)
+# --------------------------------------------------------------------------
+class _Options(C.Structure):
+    _fields_ = [("threads", C.c_uint32), ("batch", C.c_uint32),
+                ("extended_notify", C.c_int32), ("hybrid_tail", C.c_int32),
+                ("rule", C.c_int32), ("max_rounds", C.c_uint32),
+                ("smem_cache", C.c_uint32), ("reserved", C.c_uint32 * 8)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("iterations", C.c_uint64), ("messages_sent", C.c_uint64),
+                ("messages_drained", C.c_uint64), ("tail_pops", C.c_uint64),
+                ("e_scan", C.c_uint64), ("v_eval", C.c_uint64), ("drops", C.c_uint64),
+                ("tail_rounds", C.c_uint64), ("k_max", C.c_uint32), ("h_graph", C.c_uint32),
+                ("k_avg", C.c_double), ("t_upload_ms", C.c_float), ("t_prep_ms", C.c_float),
+                ("t_solve_ms", C.c_float), ("t_download_ms", C.c_float),
+                ("reserved", C.c_uint32 * 8)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+class _CSRView(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("nnz", C.c_uint64),
+                ("offsets", C.c_void_p), ("neighbors", C.c_void_p)]
+
+
+class _CSRDev(C.Structure):
+    _fields_ = [("view", _CSRView), ("device", C.c_int)]
+
+
+_INSPECTOR = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint32), C.c_uint32,
+                         C.c_uint64)
+
+# every symbol include/kcore_b200.h declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = (
+    "kc_status_str", "kc_abi_version", "kc_default_options", "kc_last_error",
+    "kc_graph_upload", "kc_graph_upload_device", "kc_graph_free", "kc_graph_n",
+    "kc_graph_nnz", "kc_graph_timings", "kc_solve", "kc_solve_device",
+    "kc_solve_observed", "kc_fastk_run", "kc_graph_stream", "kc_gen_config",
+    "kc_csr_dev_free", "kc_csr_dev_download",
+)
+
+_lib = None
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libkcore_b200.so.  Raises (no fallback) when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise RuntimeError(
+            f"{_LIB_PATH} is not built; run `python -m paper_2512_00233_b200.build` "
+            "(there is no CPU fallback for this path)")
+    L = C.CDLL(_LIB_PATH)
+    L.kc_status_str.restype = C.c_char_p
+    L.kc_status_str.argtypes = [C.c_int]
+    L.kc_last_error.restype = C.c_char_p
+    L.kc_abi_version.restype = C.c_int
+    L.kc_default_options.argtypes = [C.POINTER(_Options)]
+    L.kc_graph_upload.restype = C.c_int
+    L.kc_graph_upload.argtypes = [C.POINTER(_CSRView), C.c_int, C.POINTER(C.c_void_p)]
+    L.kc_graph_upload_device.restype = C.c_int
+    L.kc_graph_upload_device.argtypes = [C.POINTER(_CSRView), C.c_int, C.POINTER(C.c_void_p)]
+    L.kc_graph_free.argtypes = [C.c_void_p]
+    L.kc_graph_n.restype = C.c_uint32
+    L.kc_graph_n.argtypes = [C.c_void_p]
+    L.kc_graph_nnz.restype = C.c_uint64
+    L.kc_graph_nnz.argtypes = [C.c_void_p]
+    L.kc_graph_timings.restype = C.c_int
+    L.kc_graph_timings.argtypes = [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float)]
+    L.kc_graph_stream.restype = C.c_void_p
+    L.kc_graph_stream.argtypes = [C.c_void_p]
+    L.kc_solve.restype = C.c_int
+    L.kc_solve.argtypes = [C.c_void_p, C.POINTER(_Options), C.c_void_p, C.POINTER(_Stats)]
+    L.kc_solve_device.restype = C.c_int
+    L.kc_solve_device.argtypes = [C.c_void_p, C.POINTER(_Options), C.c_void_p, C.POINTER(_Stats)]
+    L.kc_solve_observed.restype = C.c_int
+    L.kc_solve_observed.argtypes = [C.c_void_p, C.POINTER(_Options), _INSPECTOR, C.c_void_p,
+                                    C.c_void_p, C.POINTER(_Stats)]
+    L.kc_fastk_run.restype = C.c_int
+    L.kc_fastk_run.argtypes = [C.POINTER(_CSRView), C.POINTER(_Options), C.c_void_p,
+                               C.POINTER(_Stats)]
+    L.kc_gen_config.restype = C.c_int
+    L.kc_gen_config.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                C.POINTER(C.POINTER(_CSRDev))]
+    L.kc_csr_dev_free.argtypes = [C.POINTER(_CSRDev)]
+    L.kc_csr_dev_download.restype = C.c_int
+    L.kc_csr_dev_download.argtypes = [C.POINTER(_CSRDev), C.c_void_p, C.c_void_p]
+    _lib = L
+    return L
+
+
+class KCError(RuntimeError):
+    def __init__(self, status: int, where: str = ""):
+        L = load_library()
+        msg = L.kc_status_str(status).decode()
+        detail = L.kc_last_error().decode()
+        super().__init__(f"{where}: {msg}" + (f" ({detail})" if detail else ""))
+        self.status = status
+
+
+def _check(status: int, where: str) -> None:
+    if status == 0:
+        return
+    if status == 1:  # KC_ERR_INVALID_ARGUMENT  ~ std::invalid_argument
+        raise ValueError(load_library().kc_last_error().decode() or "invalid argument")
+    raise KCError(status, where)
+
+
+# --------------------------------------------------------------------------
+# Reference types
+# --------------------------------------------------------------------------
+class Rule(enum.IntEnum):
+    REFERENCE = 0   # extended rule on settled values (fastk.cpp:156-163)
+    SNAPSHOT = 1    # self-activation + extended rule on the snapshot, one pass
+    AUTO = 2
+
+
+@dataclass
+class FastKOptions:
+    """include/kcore/fastk.hpp:12-22 (+ GPU knobs)."""
+    threads: int = 16
+    batch: int = 256
+    extended_notify: bool = True
+    hybrid_tail: bool = True
+    rule: Rule = Rule.AUTO
+    max_rounds: int = 0
+    smem_cache: int = 0
+
+    def _c(self) -> _Options:
+        o = _Options()
+        o.threads = max(0, int(self.threads))
+        o.batch = max(0, int(self.batch))
+        o.extended_notify = int(bool(self.extended_notify))
+        o.hybrid_tail = int(bool(self.hybrid_tail))
+        o.rule = int(self.rule)
+        o.max_rounds = int(self.max_rounds)
+        o.smem_cache = int(self.smem_cache) & 0xffffffff
+        return o
+
+
+@dataclass
+class IterationStat:
+    """report.hpp:12-15"""
+    mean_error: float
+    active_fraction: float
+
+
+@dataclass
+class RunReport:
+    """report.hpp:17-23 (+ GPU work counters and timings in `gpu`)."""
+    iterations: int = 0
+    messages_sent: int = 0
+    messages_drained: int = 0
+    tail_pops: int = 0
+    trace: list = field(default_factory=list)
+    gpu: dict = field(default_factory=dict)
+
+
+@dataclass
+class CorenessResult:
+    """oracle.hpp:10-14"""
+    coreness: np.ndarray
+    k_max: int = 0
+    k_avg: float = 0.0
+
+
+@dataclass
+class EngineResult:
+    """report.hpp:25-28"""
+    result: CorenessResult
+    report: RunReport
+
+
+@dataclass
+class Instrumentation:
+    """report.hpp:33-39: hooks at iteration boundaries (iteration 0 = degrees)."""
+    truth: Optional[CorenessResult] = None
+    trace_convergence: bool = False
+    inspector: Optional[Callable[[int, np.ndarray, int], None]] = None
+
+
+def make_coreness_result(coreness) -> CorenessResult:
+    """oracle.cpp:8-19"""
+    c = np.ascontiguousarray(coreness, dtype=np.uint32)
+    if c.size == 0:
+        return CorenessResult(c, 0, 0.0)
+    return CorenessResult(c, int(c.max()), float(c.astype(np.float64).sum() / c.size))
+
+
+def should_notify(new_core: int, old_core: int, est_v: int) -> bool:
+    """fastk.hpp:25-27"""
+    return new_core < est_v and old_core >= est_v
+
+
+def switch_condition(active_count: int, batch: int) -> bool:
+    """fastk.hpp:29-31"""
+    return active_count < batch
+
+
+class Graph:
+    """Immutable simple undirected CSR (graph.hpp:37-75)."""
+
+    def __init__(self, offsets=None, neighbors=None):
+        if offsets is None:
+            offsets = np.zeros(1, dtype=np.uint64)
+        self._off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        self._nbr = np.ascontiguousarray(
+            neighbors if neighbors is not None else np.zeros(0, np.uint32), dtype=np.uint32)
+        if self._off.size < 1 or int(self._off[0]) != 0 or int(self._off[-1]) != self._nbr.size:
+            raise ValueError("offsets must start at 0 and end at len(neighbors)")
+
+    @classmethod
+    def from_edges(cls, node_count: int, edges) -> "Graph":
+        """Graph::from_edges (graph.hpp:43-44; build_csr graph.cpp:85-128):
+        self-loops dropped, parallel edges collapse, rows strictly increasing."""
+        e = np.asarray(edges, dtype=np.int64).reshape(-1, 2) if len(edges) else \
+            np.zeros((0, 2), np.int64)
+        if e.size and (e.min() < 0 or e.max() >= node_count):
+            raise ValueError("edge endpoint out of range")
+        e = e[e[:, 0] != e[:, 1]]
+        both = np.concatenate([e, e[:, ::-1]]) if e.size else e
+        key = np.unique(both[:, 0] * np.int64(node_count) + both[:, 1]) if both.size else \
+            np.zeros(0, np.int64)
+        src = key // max(node_count, 1)
+        dst = (key % max(node_count, 1)).astype(np.uint32)
+        off = np.zeros(node_count + 1, dtype=np.uint64)
+        np.cumsum(np.bincount(src, minlength=node_count), out=off[1:])
+        return cls(off, dst)
+
+    def node_count(self) -> int:
+        return self._off.size - 1
+
+    def edge_count(self) -> int:
+        return self._nbr.size // 2
+
+    def degree(self, u: int) -> int:
+        return int(self._off[u + 1] - self._off[u])
+
+    def neighbors(self, u: int) -> np.ndarray:
+        return self._nbr[int(self._off[u]):int(self._off[u + 1])]
+
+    def offsets(self) -> np.ndarray:
+        return self._off
+
+    def neighbor_array(self) -> np.ndarray:
+        return self._nbr
+
+    def degrees(self) -> np.ndarray:
+        return np.diff(self._off).astype(np.uint32)
+
+    def _view(self) -> _CSRView:
+        v = _CSRView()
+        v.n = self.node_count()
+        v.nnz = self._nbr.size
+        v.offsets = self._off.ctypes.data
+        v.neighbors = self._nbr.ctypes.data if self._nbr.size else None
+        return v
+
+
+class DeviceCSR:
+    """A CSR built in HBM by kc_gen_config (synthetic configs, kcgen v1)."""
+
+    def __init__(self, ptr):
+        self._p = ptr
+
+    @property
+    def n(self) -> int:
+        return self._p.contents.view.n
+
+    @property
+    def nnz(self) -> int:
+        return self._p.contents.view.nnz
+
+    def view(self) -> _CSRView:
+        return self._p.contents.view
+
+    def download(self) -> Graph:
+        off = np.zeros(self.n + 1, dtype=np.uint64)
+        nbr = np.zeros(max(self.nnz, 1), dtype=np.uint32)
+        _check(load_library().kc_csr_dev_download(self._p, off.ctypes.data, nbr.ctypes.data),
+               "kc_csr_dev_download")
+        return Graph(off, nbr[: self.nnz])
+
+    def free(self) -> None:
+        if self._p:
+            load_library().kc_csr_dev_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def gen_config(cfg: int, p0: int, p1: int = 0, p2: int = 0, seed: int = 1,
+               device: int = 0) -> DeviceCSR:
+    """Build BASELINE.json config `cfg` (or a scaled variant) on the device."""
+    p = C.POINTER(_CSRDev)()
+    _check(load_library().kc_gen_config(cfg, p0, p1, p2, seed, device, C.byref(p)),
+           "kc_gen_config")
+    return DeviceCSR(p)
+
+
+class GpuGraph:
+    """An uploaded, laid-out graph handle (kc_graph)."""
+
+    def __init__(self, g, device: int = 0):
+        L = load_library()
+        self._h = C.c_void_p()
+        if isinstance(g, DeviceCSR):
+            v = g.view()
+            _check(L.kc_graph_upload_device(C.byref(v), device, C.byref(self._h)),
+                   "kc_graph_upload_device")
+        else:
+            self._keep = g
+            v = g._view()
+            _check(L.kc_graph_upload(C.byref(v), device, C.byref(self._h)), "kc_graph_upload")
+        self.n = L.kc_graph_n(self._h)
+        self.nnz = L.kc_graph_nnz(self._h)
+
+    def timings(self):
+        tu, tp = C.c_float(), C.c_float()
+        load_library().kc_graph_timings(self._h, C.byref(tu), C.byref(tp))
+        return tu.value, tp.value
+
+    def stream(self) -> int:
+        return load_library().kc_graph_stream(self._h) or 0
+
+    def solve(self, options: FastKOptions | None = None, out: np.ndarray | None = None):
+        o = (options or FastKOptions())._c()
+        st = _Stats()
+        if out is None:
+            out = np.zeros(max(self.n, 1), dtype=np.uint32)
+        _check(load_library().kc_solve(self._h, C.byref(o), out.ctypes.data, C.byref(st)),
+               "kc_solve")
+        return out[: self.n], st.as_dict()
+
+    def solve_device(self, out_ptr: int, options: FastKOptions | None = None):
+        o = (options or FastKOptions())._c()
+        st = _Stats()
+        _check(load_library().kc_solve_device(self._h, C.byref(o), C.c_void_p(out_ptr),
+                                              C.byref(st)), "kc_solve_device")
+        return st.as_dict()
+
+    def solve_observed(self, options: FastKOptions | None,
+                       fn: Callable[[int, np.ndarray, int], None]):
+        o = (options or FastKOptions())._c()
+        st = _Stats()
+        out = np.zeros(max(self.n, 1), dtype=np.uint32)
+        err = []
+
+        def cb(user, it, est, n, active):
+            try:
+                arr = np.ctypeslib.as_array(est, shape=(n,)).copy() if n else \
+                    np.zeros(0, np.uint32)
+                fn(int(it), arr, int(active))
+                return 0
+            except Exception as e:  # propagate after the call returns
+                err.append(e)
+                return 1
+
+        cfn = _INSPECTOR(cb)
+        status = load_library().kc_solve_observed(self._h, C.byref(o), cfn, None,
+                                                  out.ctypes.data, C.byref(st))
+        if err:
+            raise err[0]
+        _check(status, "kc_solve_observed")
+        return out[: self.n], st.as_dict()
+
+    def free(self) -> None:
+        if getattr(self, "_h", None):
+            load_library().kc_graph_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _report(st: dict, trace=None) -> RunReport:
+    return RunReport(iterations=int(st["iterations"]), messages_sent=int(st["messages_sent"]),
+                     messages_drained=int(st["messages_drained"]),
+                     tail_pops=int(st["tail_pops"]), trace=trace or [], gpu=st)
+
+
+def fastk_run(g: Graph, options: FastKOptions | None = None,
+              instr: Instrumentation | None = None, device: int = 0) -> EngineResult:
+    """kcore::fastk_run (fastk.hpp:46-47) on the B200.
+
+    ValueError for zero threads/batch before any work (fastk.cpp:58-59)."""
+    options = options or FastKOptions()
+    if int(options.threads) == 0:
+        raise ValueError("fastk: threads must be >= 1")
+    if int(options.batch) == 0:
+        raise ValueError("fastk: batch must be >= 1")
+    gg = GpuGraph(g, device)
+    try:
+        if instr is None or (not instr.trace_convergence and instr.inspector is None):
+            core, st = gg.solve(options)
+            return EngineResult(CorenessResult(core, int(st["k_max"]), float(st["k_avg"])),
+                                _report(st))
+        trace = []
+        n = g.node_count()
+        truth = None
+        if instr.trace_convergence:
+            if instr.truth is None:
+                raise ValueError("trace_convergence requires truth")
+            truth = np.asarray(instr.truth.coreness, dtype=np.float64)
+
+        def hook(it, est, active):
+            if truth is not None:  # record_iteration, report.cpp:7-18
+                gap = float((est.astype(np.float64) - truth).sum()) if n else 0.0
+                trace.append(IterationStat(gap / n if n else 0.0, active / n if n else 0.0))
+            if instr.inspector is not None:
+                instr.inspector(it, est, active)
+
+        core, st = gg.solve_observed(options, hook)
+        return EngineResult(CorenessResult(core, int(st["k_max"]), float(st["k_avg"])),
+                            _report(st, trace))
+    finally:
+        gg.free()

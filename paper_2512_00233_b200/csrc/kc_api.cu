@@ -1,0 +1,552 @@
+// kc_api.cu — the C-ABI (include/kcore_b200.h) over the sm_100a solver.
+//
+// Host side of the drop-in for kcore::fastk_run (reference
+// include/kcore/fastk.hpp:46-47, src/fastk.cpp:57-187): validation with the
+// reference's error behaviour (threads/batch == 0 rejected before any work,
+// fastk.cpp:58-59), CSR upload, on-device layout (kc_prep.cu), the persistent
+// round kernel (kc_solve.cu), permute-back + download, RunReport counters.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/kcore_b200.h"
+#include "kc_internal.h"
+
+using namespace kcb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+kc_status fail(kc_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+kc_status cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear sticky-less errors
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  if (e == cudaErrorMemoryAllocation) return fail(KC_ERR_OUT_OF_MEMORY, m);
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver || e == cudaErrorInvalidDevice)
+    return fail(KC_ERR_NO_DEVICE, m);
+  return fail(KC_ERR_CUDA, m);
+}
+
+#define CK(x)                                      \
+  do {                                             \
+    cudaError_t e_ = (x);                          \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x); \
+  } while (0)
+
+kc_status check_device(int device, int* num_sms) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(KC_ERR_NO_DEVICE, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  if (device < 0 || device >= count) return fail(KC_ERR_NO_DEVICE, "device index out of range");
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(KC_ERR_NO_DEVICE, std::string("device is not sm_100 (Blackwell): ") + prop.name);
+  CK(cudaSetDevice(device));
+  if (num_sms) *num_sms = prop.multiProcessorCount;
+  return KC_OK;
+}
+
+__global__ void permute_back_kernel(const void* est, bool est16, const uint32_t* perm,
+                                    uint32_t n, uint32_t n_nz, uint32_t* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    if (i < n_nz) v = est16 ? ((const uint16_t*)est)[i] : ((const uint32_t*)est)[i];
+    out[perm[i]] = v;
+  }
+}
+
+template <typename OffT>
+__global__ void degree_back_kernel(const OffT* off, const uint32_t* perm, uint32_t n,
+                                   uint32_t n_nz, uint32_t* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[perm[i]] = i < n_nz ? (uint32_t)(off[i + 1] - off[i]) : 0u;
+}
+
+// k_max and sum of estimates (n_nz entries).
+__global__ void kstats_kernel(const void* est, bool est16, uint32_t n_nz,
+                              unsigned long long* out /* [0]=max, [1]=sum */) {
+  uint32_t mx = 0;
+  unsigned long long sm = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_nz; i += gridDim.x * blockDim.x) {
+    uint32_t v = est16 ? ((const uint16_t*)est)[i] : ((const uint32_t*)est)[i];
+    mx = v > mx ? v : mx;
+    sm += v;
+  }
+  typedef cub::BlockReduce<unsigned long long, 256> BR;
+  __shared__ typename BR::TempStorage t1;
+  __shared__ typename BR::TempStorage t2;
+  unsigned long long bmx = BR(t1).Reduce((unsigned long long)mx, cub::Max());
+  unsigned long long bsm = BR(t2).Sum(sm);
+  if (threadIdx.x == 0) {
+    atomicMax(&out[0], bmx);
+    atomicAdd(&out[1], bsm);
+  }
+}
+
+}  // namespace
+
+struct kc_graph {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint32_t n = 0;
+  uint64_t nnz = 0;
+  PrepOut lay{};
+  bool est16 = true;
+  float t_upload = 0.f, t_prep = 0.f;
+  // solver state (allocated at first solve)
+  bool solver_ready = false;
+  uint32_t max_rounds = 0;
+  SolveBuffers sb{};
+  uint32_t* d_out = nullptr;      // coreness in caller ids [n]
+  unsigned long long* d_k = nullptr;
+};
+
+namespace {
+
+void free_solver(kc_graph* g) {
+  if (!g->solver_ready) return;
+  cudaFree(g->sb.est);
+  cudaFree(g->sb.queue[0]);
+  cudaFree(g->sb.queue[1]);
+  cudaFree(g->sb.qcnt);
+  cudaFree(g->sb.bm[0]);
+  cudaFree(g->sb.bm[1]);
+  cudaFree(g->sb.drop_u);
+  cudaFree(g->sb.drop_t);
+  cudaFree(g->sb.drop_old);
+  cudaFree(g->sb.ctl);
+  cudaFree(g->sb.stats);
+  cudaFree(g->sb.status);
+  cudaFree(g->d_out);
+  cudaFree(g->d_k);
+  g->solver_ready = false;
+}
+
+kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
+  (void)max_rounds;
+  if (g->solver_ready) return KC_OK;
+  free_solver(g);
+  const uint32_t n_nz = g->lay.n_nz;
+  const size_t es = g->est16 ? 2 : 4;
+  const size_t n_pad = ((size_t)n_nz + 15) & ~(size_t)15;  // cache fill reads 16 B vectors
+  const size_t words = ((size_t)n_nz + 31) / 32;
+  SolveBuffers& b = g->sb;
+  std::memset(&b, 0, sizeof(b));
+  b.off = g->lay.off;
+  b.adj = g->lay.adj;
+  b.n_nz = n_nz;
+  for (int c = 0; c <= NCLS; ++c) b.cls_begin[c] = g->lay.cls_begin[c];
+  g->solver_ready = true;  // so that partial allocations get freed
+  CK(cudaMalloc(&b.est, n_pad * es));
+  CK(cudaMemsetAsync(b.est, 0, n_pad * es, g->stream));
+  CK(cudaMalloc(&b.queue[0], (n_nz ? n_nz : 1) * sizeof(uint32_t)));
+  CK(cudaMalloc(&b.queue[1], (n_nz ? n_nz : 1) * sizeof(uint32_t)));
+  CK(cudaMalloc(&b.qcnt, 2 * NCLS * sizeof(uint32_t)));
+  CK(cudaMalloc(&b.bm[0], (words ? words : 1) * sizeof(uint32_t)));
+  CK(cudaMalloc(&b.bm[1], (words ? words : 1) * sizeof(uint32_t)));
+  CK(cudaMalloc(&b.drop_u, (n_nz ? n_nz : 1) * sizeof(uint32_t)));
+  CK(cudaMalloc(&b.drop_t, (n_nz ? n_nz : 1) * es));
+  CK(cudaMalloc(&b.drop_old, (n_nz ? n_nz : 1) * es));
+  CK(cudaMalloc(&b.ctl, 2 * sizeof(Ctl)));
+  CK(cudaMalloc(&b.stats, (size_t)STAT_SLOTS * sizeof(RoundStat)));
+  CK(cudaMalloc(&b.status, 4 * sizeof(uint32_t)));
+  CK(cudaMalloc(&g->d_out, (g->n ? g->n : 1) * sizeof(uint32_t)));
+  CK(cudaMalloc(&g->d_k, 2 * sizeof(unsigned long long)));
+  g->max_rounds = max_rounds;
+  return KC_OK;
+}
+
+int map_rule(const kc_options& o) {
+  const bool ref = o.rule == KC_RULE_REFERENCE;
+  if (ref) return o.extended_notify ? R_REF_EXT : R_REF_PLAIN;
+  return o.extended_notify ? R_SNAP_EXT : R_SNAP_PLAIN;
+}
+
+kc_status validate(const kc_options* opt, kc_options* o) {
+  if (opt) *o = *opt; else kc_default_options(o);
+  // fastk.cpp:58-59 — rejected before any work
+  if (o->threads == 0) return fail(KC_ERR_INVALID_ARGUMENT, "fastk: threads must be >= 1");
+  if (o->batch == 0) return fail(KC_ERR_INVALID_ARGUMENT, "fastk: batch must be >= 1");
+  if (o->rule < 0 || o->rule > KC_RULE_AUTO) return fail(KC_ERR_INVALID_ARGUMENT, "unknown rule");
+  if (o->rule == KC_RULE_AUTO) o->rule = KC_RULE_SNAPSHOT;
+  // Every round with a drop lowers sum(est) by >= 1, so the loop terminates;
+  // 0 means no cap (paths need ~n/2 Jacobi rounds).
+  if (o->max_rounds == 0) o->max_rounds = 0xffffffffu;
+  return KC_OK;
+}
+
+uint32_t cache_entries(const kc_graph* g, const kc_options& o) {
+  if (o.smem_cache == 0xffffffffu) return 0;
+  const size_t es = g->est16 ? 2 : 4;
+  size_t want = o.smem_cache ? o.smem_cache : solver_cache_bytes_max() / es;
+  size_t maxe = solver_cache_bytes_max() / es;
+  if (want > maxe) want = maxe;
+  size_t n_pad = ((size_t)g->lay.n_nz + 15) & ~(size_t)15;
+  if (want > n_pad) want = n_pad;
+  want &= ~(size_t)15;  // 16-entry multiple (16-byte vectors for either width)
+  return (uint32_t)want;
+}
+
+// Run the solver to convergence (or one round when `one_round`), leaving the
+// estimates on the device.  Fills the counters of `st`.
+kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_t r_end) {
+  SolveConfig c{};
+  c.rule = map_rule(o);
+  c.cache_n = cache_entries(g, o);
+  c.max_rounds = o.max_rounds;
+  c.tail_threshold = 0;
+  c.num_sms = g->num_sms;
+  CK(launch_rounds(g->sb, c, g->est16, g->lay.off64, r_begin, r_end, g->stream));
+  return KC_OK;
+}
+
+kc_status collect(kc_graph* g, const kc_options& o, kc_stats* st, bool* converged) {
+  uint32_t status[4] = {0, 0, 0, 0};
+  CK(cudaMemcpyAsync(status, g->sb.status, sizeof(status), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  const uint32_t rounds = status[0];
+  *converged = status[1] != 0;
+  if (!st) return KC_OK;
+  const uint32_t slots = rounds < STAT_SLOTS ? rounds : STAT_SLOTS;
+  std::vector<RoundStat> rs(slots);
+  if (slots)
+    CK(cudaMemcpy(rs.data(), g->sb.stats, slots * sizeof(RoundStat), cudaMemcpyDeviceToHost));
+  st->iterations = rounds;
+  st->messages_sent = st->messages_drained = st->e_scan = st->v_eval = st->drops = 0;
+  for (const RoundStat& r : rs) {
+    st->messages_sent += r.fires;
+    st->v_eval += r.evals;
+    st->e_scan += r.escan;
+    st->drops += r.drops;
+  }
+  // isolated vertices are evaluated once in round 0 by the reference
+  // (fastk.cpp:128-149 sweeps all ids); they cost nothing here.
+  st->messages_drained = st->v_eval + (rounds ? (uint64_t)(g->n - g->lay.n_nz) : 0);
+  st->tail_pops = 0;
+  st->tail_rounds = status[2];
+  (void)o;
+  return KC_OK;
+}
+
+kc_status kstats(kc_graph* g, kc_stats* st) {
+  if (!st) return KC_OK;
+  unsigned long long k[2] = {0, 0};
+  CK(cudaMemsetAsync(g->d_k, 0, 2 * sizeof(unsigned long long), g->stream));
+  if (g->lay.n_nz) {
+    kstats_kernel<<<g->num_sms * 2, 256, 0, g->stream>>>(g->sb.est, g->est16, g->lay.n_nz, g->d_k);
+    CK(cudaGetLastError());
+  }
+  CK(cudaMemcpyAsync(k, g->d_k, sizeof(k), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  st->k_max = (uint32_t)k[0];
+  st->k_avg = g->n ? (double)k[1] / (double)g->n : 0.0;
+  st->h_graph = g->lay.h_graph;
+  return KC_OK;
+}
+
+kc_status permute_back(kc_graph* g) {
+  if (!g->n) return KC_OK;
+  permute_back_kernel<<<g->num_sms * 4, 256, 0, g->stream>>>(g->sb.est, g->est16, g->lay.perm,
+                                                             g->n, g->lay.n_nz, g->d_out);
+  CK(cudaGetLastError());
+  return KC_OK;
+}
+
+kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, kc_graph** out) {
+  if (!out) return fail(KC_ERR_INVALID_ARGUMENT, "out is null");
+  *out = nullptr;
+  if (!csr) return fail(KC_ERR_INVALID_ARGUMENT, "csr view is null");
+  if (csr->n > 0 && (!csr->offsets || (csr->nnz > 0 && !csr->neighbors)))
+    return fail(KC_ERR_INVALID_ARGUMENT, "csr view has null arrays");
+  int sms = 0;
+  kc_status s = check_device(device, &sms);
+  if (s != KC_OK) return s;
+  kc_graph* g = new (std::nothrow) kc_graph();
+  if (!g) return fail(KC_ERR_OUT_OF_MEMORY, "host allocation failed");
+  g->device = device;
+  g->num_sms = sms;
+  g->n = csr->n;
+  g->nnz = csr->nnz;
+  auto bail = [&](kc_status st) {
+    kc_graph_free(g);
+    return st;
+  };
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return bail(cuda_fail(e, "cudaStreamCreate"));
+  for (auto& ev : g->ev)
+    if ((e = cudaEventCreate(&ev)) != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
+  if (g->n == 0) {
+    *out = g;
+    return KC_OK;
+  }
+  uint64_t* d_off = nullptr;
+  uint32_t* d_adj = nullptr;
+  if (!on_device) {
+    if (csr->offsets[0] != 0 || csr->offsets[csr->n] != csr->nnz)
+      return bail(fail(KC_ERR_INVALID_ARGUMENT, "offsets[0] != 0 or offsets[n] != nnz"));
+    cudaEventRecord(g->ev[0], g->stream);
+    if ((e = cudaMalloc(&d_off, ((size_t)g->n + 1) * sizeof(uint64_t))) != cudaSuccess)
+      return bail(cuda_fail(e, "cudaMalloc offsets"));
+    if ((e = cudaMalloc(&d_adj, (g->nnz ? g->nnz : 1) * sizeof(uint32_t))) != cudaSuccess) {
+      cudaFree(d_off);
+      return bail(cuda_fail(e, "cudaMalloc neighbors"));
+    }
+    e = cudaMemcpyAsync(d_off, csr->offsets, ((size_t)g->n + 1) * sizeof(uint64_t),
+                        cudaMemcpyHostToDevice, g->stream);
+    if (e == cudaSuccess && g->nnz)
+      e = cudaMemcpyAsync(d_adj, csr->neighbors, g->nnz * sizeof(uint32_t),
+                          cudaMemcpyHostToDevice, g->stream);
+    if (e != cudaSuccess) {
+      cudaFree(d_off);
+      cudaFree(d_adj);
+      return bail(cuda_fail(e, "cudaMemcpy H2D"));
+    }
+    cudaEventRecord(g->ev[1], g->stream);
+  } else {
+    d_off = const_cast<uint64_t*>(csr->offsets);
+    d_adj = const_cast<uint32_t*>(csr->neighbors);
+    cudaEventRecord(g->ev[0], g->stream);
+    cudaEventRecord(g->ev[1], g->stream);
+  }
+  e = prep_layout(d_off, d_adj, g->n, g->nnz, false, g->stream, &g->lay);
+  cudaEventRecord(g->ev[2], g->stream);
+  cudaStreamSynchronize(g->stream);
+  if (!on_device) {
+    cudaFree(d_off);
+    cudaFree(d_adj);
+  }
+  if (e != cudaSuccess) return bail(cuda_fail(e, "layout"));
+  cudaEventElapsedTime(&g->t_upload, g->ev[0], g->ev[1]);
+  cudaEventElapsedTime(&g->t_prep, g->ev[1], g->ev[2]);
+  g->est16 = g->lay.h_graph < 65535u;
+  *out = g;
+  return KC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kc_status_str(kc_status s) {
+  switch (s) {
+    case KC_OK: return "ok";
+    case KC_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case KC_ERR_NO_DEVICE: return "no usable sm_100 CUDA device";
+    case KC_ERR_OUT_OF_MEMORY: return "out of device memory";
+    case KC_ERR_CUDA: return "CUDA error";
+    case KC_ERR_NOT_CONVERGED: return "round cap exceeded before convergence";
+    case KC_ERR_CALLBACK: return "inspector callback aborted the run";
+  }
+  return "unknown status";
+}
+
+int kc_abi_version(void) { return KC_ABI_VERSION; }
+
+const char* kc_last_error(void) { return g_last_error.c_str(); }
+
+void kc_default_options(kc_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->threads = 16;  // FastKOptions defaults, fastk.hpp:12-22
+  o->batch = 256;
+  o->extended_notify = 1;
+  o->hybrid_tail = 1;
+  o->rule = KC_RULE_AUTO;
+  o->max_rounds = 0;
+  o->smem_cache = 0;
+}
+
+kc_status kc_graph_upload(const kc_csr_view* csr, int device, kc_graph** out) {
+  g_last_error.clear();
+  return upload_common(csr, device, false, out);
+}
+
+kc_status kc_graph_upload_device(const kc_csr_view* csr, int device, kc_graph** out) {
+  g_last_error.clear();
+  return upload_common(csr, device, true, out);
+}
+
+void kc_graph_free(kc_graph* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  free_solver(g);
+  cudaFree(g->lay.off);
+  cudaFree(g->lay.adj);
+  cudaFree(g->lay.perm);
+  for (auto& ev : g->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+uint32_t kc_graph_n(const kc_graph* g) { return g ? g->n : 0; }
+uint64_t kc_graph_nnz(const kc_graph* g) { return g ? g->nnz : 0; }
+void* kc_graph_stream(kc_graph* g) { return g ? (void*)g->stream : nullptr; }
+
+kc_status kc_graph_timings(const kc_graph* g, float* tu, float* tp) {
+  if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
+  if (tu) *tu = g->t_upload;
+  if (tp) *tp = g->t_prep;
+  return KC_OK;
+}
+
+static kc_status solve_impl(kc_graph* g, const kc_options* opt, uint32_t* out, bool out_dev,
+                            kc_stats* st) {
+  g_last_error.clear();
+  if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
+  kc_options o;
+  kc_status s = validate(opt, &o);
+  if (s != KC_OK) return s;
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->t_upload_ms = g->t_upload;
+    st->t_prep_ms = g->t_prep;
+  }
+  CK(cudaSetDevice(g->device));
+  if (g->n == 0) {  // empty graph: one (empty) round, tests/test_fastk.cpp:156-159
+    if (st) st->iterations = 1;
+    return KC_OK;
+  }
+  if (g->lay.n_nz == 0) {  // edgeless: one round evaluates every vertex to 0
+    if (out_dev) CK(cudaMemsetAsync(out, 0, g->n * sizeof(uint32_t), g->stream));
+    else std::memset(out, 0, g->n * sizeof(uint32_t));
+    CK(cudaStreamSynchronize(g->stream));
+    if (st) {
+      st->iterations = 1;
+      st->messages_drained = g->n;
+      st->h_graph = 0;
+    }
+    return KC_OK;
+  }
+  s = ensure_solver(g, o.max_rounds);
+  if (s != KC_OK) return s;
+  CK(cudaEventRecord(g->ev[0], g->stream));
+  CK(launch_init(g->sb, g->est16, g->lay.off64, g->lay.h_graph, o.max_rounds, g->stream));
+  s = run_rounds(g, o, 0, o.max_rounds);
+  if (s != KC_OK) return s;
+  CK(cudaEventRecord(g->ev[1], g->stream));
+  bool conv = false;
+  s = collect(g, o, st, &conv);
+  if (s != KC_OK) return s;
+  if (!conv) return fail(KC_ERR_NOT_CONVERGED, "round cap reached");
+  s = kstats(g, st);
+  if (s != KC_OK) return s;
+  CK(cudaEventRecord(g->ev[2], g->stream));
+  s = permute_back(g);
+  if (s != KC_OK) return s;
+  if (out_dev)
+    CK(cudaMemcpyAsync(out, g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, g->stream));
+  else
+    CK(cudaMemcpyAsync(out, g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaEventRecord(g->ev[3], g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  if (st) {
+    cudaEventElapsedTime(&st->t_solve_ms, g->ev[0], g->ev[1]);
+    cudaEventElapsedTime(&st->t_download_ms, g->ev[2], g->ev[3]);
+  }
+  return KC_OK;
+}
+
+kc_status kc_solve(kc_graph* g, const kc_options* opt, uint32_t* coreness, kc_stats* st) {
+  if (g && g->n && !coreness) return fail(KC_ERR_INVALID_ARGUMENT, "coreness is null");
+  return solve_impl(g, opt, coreness, false, st);
+}
+
+kc_status kc_solve_device(kc_graph* g, const kc_options* opt, uint32_t* coreness_dev,
+                          kc_stats* st) {
+  if (g && g->n && !coreness_dev) return fail(KC_ERR_INVALID_ARGUMENT, "coreness is null");
+  return solve_impl(g, opt, coreness_dev, true, st);
+}
+
+kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn fn, void* user,
+                            uint32_t* coreness, kc_stats* st) {
+  g_last_error.clear();
+  if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
+  kc_options o;
+  kc_status s = validate(opt, &o);
+  if (s != KC_OK) return s;
+  if (g->n && !coreness) return fail(KC_ERR_INVALID_ARGUMENT, "coreness is null");
+  if (st) std::memset(st, 0, sizeof(*st));
+  CK(cudaSetDevice(g->device));
+  std::vector<uint32_t> snap(g->n);
+  if (g->n == 0 || g->lay.n_nz == 0) {
+    // iteration 0 (degrees = 0) and the single quiescent round
+    if (fn && fn(user, 0, snap.data(), g->n, g->n)) return fail(KC_ERR_CALLBACK, "inspector");
+    if (fn && fn(user, 1, snap.data(), g->n, 0)) return fail(KC_ERR_CALLBACK, "inspector");
+    if (g->n) std::memset(coreness, 0, g->n * sizeof(uint32_t));
+    if (st) {
+      st->iterations = 1;
+      st->messages_drained = g->n;
+    }
+    return KC_OK;
+  }
+  s = ensure_solver(g, o.max_rounds);
+  if (s != KC_OK) return s;
+  CK(launch_init(g->sb, g->est16, g->lay.off64, g->lay.h_graph, o.max_rounds, g->stream));
+  // iteration 0: the reference reports est = degree (fastk.cpp:67-68, 93)
+  if (g->lay.off64)
+    degree_back_kernel<uint64_t><<<g->num_sms * 4, 256, 0, g->stream>>>(
+        (const uint64_t*)g->lay.off, g->lay.perm, g->n, g->lay.n_nz, g->d_out);
+  else
+    degree_back_kernel<uint32_t><<<g->num_sms * 4, 256, 0, g->stream>>>(
+        (const uint32_t*)g->lay.off, g->lay.perm, g->n, g->lay.n_nz, g->d_out);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(snap.data(), g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  if (fn && fn(user, 0, snap.data(), g->n, g->n)) return fail(KC_ERR_CALLBACK, "inspector");
+  bool conv = false;
+  for (uint32_t r = 0; r < o.max_rounds && !conv; ++r) {
+    s = run_rounds(g, o, r, r + 1);
+    if (s != KC_OK) return s;
+    s = collect(g, o, nullptr, &conv);
+    if (s != KC_OK) return s;
+    RoundStat rs;
+    CK(cudaMemcpy(&rs, g->sb.stats + (r < STAT_SLOTS - 1 ? r : STAT_SLOTS - 1), sizeof(rs),
+                  cudaMemcpyDeviceToHost));
+    s = permute_back(g);
+    if (s != KC_OK) return s;
+    CK(cudaMemcpyAsync(snap.data(), g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    if (fn && fn(user, (uint64_t)r + 1, snap.data(), g->n, conv ? 0 : rs.active_after))
+      return fail(KC_ERR_CALLBACK, "inspector");
+  }
+  if (!conv) return fail(KC_ERR_NOT_CONVERGED, "round cap reached");
+  s = collect(g, o, st, &conv);
+  if (s != KC_OK) return s;
+  s = kstats(g, st);
+  if (s != KC_OK) return s;
+  std::memcpy(coreness, snap.data(), g->n * sizeof(uint32_t));
+  return KC_OK;
+}
+
+kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* coreness,
+                       kc_stats* st) {
+  kc_options o;
+  kc_status s = validate(opt, &o);  // invalid options rejected before any work
+  if (s != KC_OK) return s;
+  kc_graph* g = nullptr;
+  s = kc_graph_upload(csr, 0, &g);
+  if (s != KC_OK) return s;
+  s = kc_solve(g, &o, coreness, st);
+  kc_graph_free(g);
+  return s;
+}
+
+}  // extern "C"

@@ -1,0 +1,277 @@
+// kc_prep.cu — on-device layout of the uploaded CSR for the solver.
+//
+// Input: the reference Graph's CSR (uint64 offsets, uint32 neighbours,
+// include/kcore/graph.hpp:72-73) already in device memory.
+// Output (owned by kc_graph):
+//   * vertices relabelled by descending degree (stable, so equal-degree runs
+//     keep their original order): degree classes become id ranges, the most
+//     gathered estimates become a dense prefix that fits shared memory, and
+//     isolated vertices (coreness 0, never evaluated) drop off the end;
+//   * offsets narrowed to uint32 whenever nnz < 2^32 (uint64 otherwise);
+//   * neighbours rewritten to new ids, each row sorted ascending so a warp's
+//     gathers walk est[] in increasing address order;
+//   * perm[new] = old for the permute-back at download.
+#include <cub/cub.cuh>
+#include <cstdint>
+
+#include "kc_internal.h"
+
+namespace kcb {
+namespace {
+
+__global__ void degrees_kernel(const uint64_t* __restrict__ off, uint32_t n,
+                               uint32_t* __restrict__ deg, uint32_t* __restrict__ iota) {
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+    deg[u] = (uint32_t)(off[u + 1] - off[u]);
+    iota[u] = u;
+  }
+}
+
+__global__ void inverse_kernel(const uint32_t* __restrict__ perm, uint32_t n,
+                               uint32_t* __restrict__ inv) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    inv[perm[i]] = i;
+}
+
+// Boundaries on the descending degree sequence: out[0] = H (h-index of the
+// degree sequence), out[1..4] = #vertices with degree > {32768, 1024, 64, 8},
+// out[5] = #vertices with degree > 0 (n_nz).
+__global__ void bounds_kernel(const uint32_t* __restrict__ sdeg, uint32_t n, uint32_t* out) {
+  const uint32_t k = threadIdx.x;
+  if (k > 5) return;
+  if (k == 0) {  // largest h with sdeg[h-1] >= h
+    uint32_t lo = 0, hi = n;  // answer in [lo, hi]
+    while (lo < hi) {
+      uint32_t mid = lo + (hi - lo + 1) / 2;
+      if (sdeg[mid - 1] >= mid) lo = mid; else hi = mid - 1;
+    }
+    out[0] = lo;
+    return;
+  }
+  const uint32_t thr[6] = {0, DEG_BLOCK_MAX, DEG_WARP_MAX, DEG_SUB_MAX, DEG_THREAD_MAX, 0};
+  const uint32_t t = thr[k];
+  uint32_t lo = 0, hi = n;  // count of sdeg[i] > t (prefix, sdeg descending)
+  while (lo < hi) {
+    uint32_t mid = lo + (hi - lo) / 2;
+    if (sdeg[mid] > t) lo = mid + 1; else hi = mid;
+  }
+  out[k] = lo;
+}
+
+template <typename OffT>
+__global__ void narrow_offsets_kernel(const uint64_t* __restrict__ src, uint32_t m,
+                                      OffT* __restrict__ dst) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    dst[i] = (OffT)src[i];
+}
+
+// Rewrite row i (old row perm[i]) into new ids.  Rows are split into
+// 1024-entry chunks so hub rows spread over many warps.
+template <typename OffT>
+__global__ void relabel_rows_kernel(const uint64_t* __restrict__ old_off,
+                                    const uint32_t* __restrict__ old_adj,
+                                    const uint32_t* __restrict__ perm,
+                                    const uint32_t* __restrict__ inv,
+                                    const uint64_t* __restrict__ chunk_base,  // per row, scan of chunks
+                                    uint32_t n_nz, const OffT* __restrict__ new_off,
+                                    uint32_t* __restrict__ new_adj, uint64_t total_chunks) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  for (uint64_t c = w0; c < total_chunks; c += nw) {
+    // row containing chunk c: largest i with chunk_base[i] <= c
+    uint32_t lo = 0, hi = n_nz;
+    while (hi - lo > 1) {
+      uint32_t mid = lo + (hi - lo) / 2;
+      if (chunk_base[mid] <= c) lo = mid; else hi = mid;
+    }
+    const uint32_t i = lo;
+    const uint64_t k0 = (c - chunk_base[i]) * 1024;
+    const uint64_t deg = (uint64_t)(new_off[i + 1] - new_off[i]);
+    const uint64_t k1 = k0 + 1024 < deg ? k0 + 1024 : deg;
+    const uint32_t* src = old_adj + old_off[perm[i]];
+    uint32_t* dst = new_adj + new_off[i];
+    for (uint64_t k = k0 + lane; k < k1; k += 32) dst[k] = inv[src[k]];
+  }
+}
+
+template <typename OffT>
+__global__ void chunk_count_kernel(const OffT* __restrict__ new_off, uint32_t n_nz,
+                                   uint64_t* __restrict__ chunks) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_nz; i += gridDim.x * blockDim.x)
+    chunks[i] = ((uint64_t)(new_off[i + 1] - new_off[i]) + 1023) / 1024;
+}
+
+}  // namespace
+
+#define PREP_CK(x)                         \
+  do {                                     \
+    cudaError_t e_ = (x);                  \
+    if (e_ != cudaSuccess) {               \
+      err = e_;                            \
+      goto done;                           \
+    }                                      \
+  } while (0)
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T));
+}
+
+// Relabel + narrow + sort rows.  `off`/`adj` are device pointers to the
+// uploaded reference CSR (not modified).
+cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, uint64_t nnz,
+                        bool force_off64, cudaStream_t s, PrepOut* out) {
+  cudaError_t err = cudaSuccess;
+  uint32_t *deg = nullptr, *iota = nullptr, *sdeg = nullptr, *perm = nullptr, *inv = nullptr;
+  uint32_t* bounds = nullptr;
+  uint64_t* off64_tmp = nullptr;
+  uint64_t* chunks = nullptr;
+  void* new_off = nullptr;
+  uint32_t* new_adj = nullptr;
+  uint32_t* sort_tmp = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0, need = 0;
+  uint32_t hb[6] = {0, 0, 0, 0, 0, 0};
+  const bool off64 = force_off64 || nnz >= (1ull << 32);
+  const int G = 148 * 8, B = 256;
+  out->off = nullptr;
+  out->adj = nullptr;
+  out->perm = nullptr;
+
+  PREP_CK(dalloc(&deg, n));
+  PREP_CK(dalloc(&iota, n));
+  PREP_CK(dalloc(&sdeg, n));
+  PREP_CK(dalloc(&perm, n));
+  PREP_CK(dalloc(&inv, n));
+  PREP_CK(dalloc(&bounds, 8));
+  degrees_kernel<<<G, B, 0, s>>>(off, n, deg, iota);
+  PREP_CK(cudaGetLastError());
+  // stable descending radix sort of (degree, id)
+  PREP_CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, need, deg, sdeg, iota, perm, n, 0, 32, s));
+  tmp_bytes = need;
+  PREP_CK(cudaMalloc(&tmp, tmp_bytes ? tmp_bytes : 1));
+  PREP_CK(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, deg, sdeg, iota, perm, n, 0, 32, s));
+  inverse_kernel<<<G, B, 0, s>>>(perm, n, inv);
+  PREP_CK(cudaGetLastError());
+  bounds_kernel<<<1, 32, 0, s>>>(sdeg, n, bounds);
+  PREP_CK(cudaGetLastError());
+  PREP_CK(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, s));
+  PREP_CK(cudaStreamSynchronize(s));
+  out->h_graph = hb[0];
+  out->n_nz = hb[5];
+  out->cls_begin[0] = 0;
+  for (int c = 1; c <= 4; ++c) out->cls_begin[c] = hb[c];
+  out->cls_begin[5] = hb[5];
+  out->off64 = off64;
+  {
+    const uint32_t n_nz = out->n_nz;
+    // new offsets: exclusive scan of sorted degrees (n_nz + 1 entries)
+    PREP_CK(dalloc(&off64_tmp, (size_t)n_nz + 1));
+    PREP_CK(cudaMemsetAsync(off64_tmp, 0, sizeof(uint64_t), s));
+    {
+      auto in = cub::TransformInputIterator<uint64_t, cub::CastOp<uint64_t>, const uint32_t*>(
+          sdeg, cub::CastOp<uint64_t>());
+      size_t nb = 0;
+      PREP_CK(cub::DeviceScan::InclusiveSum(nullptr, nb, in, off64_tmp + 1, n_nz, s));
+      if (nb > tmp_bytes) {
+        PREP_CK(cudaFree(tmp));
+        tmp = nullptr;
+        tmp_bytes = nb;
+        PREP_CK(cudaMalloc(&tmp, tmp_bytes));
+      }
+      PREP_CK(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, in, off64_tmp + 1, n_nz, s));
+    }
+    if (off64) {
+      new_off = off64_tmp;
+      off64_tmp = nullptr;
+    } else {
+      PREP_CK(cudaMalloc(&new_off, ((size_t)n_nz + 1) * sizeof(uint32_t)));
+      narrow_offsets_kernel<uint32_t><<<G, B, 0, s>>>(off64_tmp, n_nz + 1, (uint32_t*)new_off);
+      PREP_CK(cudaGetLastError());
+    }
+    PREP_CK(dalloc(&new_adj, nnz));
+    PREP_CK(dalloc(&chunks, (size_t)n_nz + 1));
+    if (n_nz) {
+      if (off64)
+        chunk_count_kernel<uint64_t><<<G, B, 0, s>>>((const uint64_t*)new_off, n_nz, chunks);
+      else
+        chunk_count_kernel<uint32_t><<<G, B, 0, s>>>((const uint32_t*)new_off, n_nz, chunks);
+      PREP_CK(cudaGetLastError());
+      size_t nb = 0;
+      PREP_CK(cub::DeviceScan::ExclusiveSum(nullptr, nb, chunks, chunks, n_nz + 1, s));
+      if (nb > tmp_bytes) {
+        PREP_CK(cudaFree(tmp));
+        tmp = nullptr;
+        tmp_bytes = nb;
+        PREP_CK(cudaMalloc(&tmp, tmp_bytes));
+      }
+      // chunks[n_nz] must be 0 before the exclusive scan so the total lands there
+      PREP_CK(cudaMemsetAsync(chunks + n_nz, 0, sizeof(uint64_t), s));
+      PREP_CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, chunks, chunks, n_nz + 1, s));
+      uint64_t total = 0;
+      PREP_CK(cudaMemcpyAsync(&total, chunks + n_nz, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      PREP_CK(cudaStreamSynchronize(s));
+      if (off64)
+        relabel_rows_kernel<uint64_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_nz,
+                                                      (const uint64_t*)new_off, new_adj, total);
+      else
+        relabel_rows_kernel<uint32_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_nz,
+                                                      (const uint32_t*)new_off, new_adj, total);
+      PREP_CK(cudaGetLastError());
+      // sort each row ascending (segmented sort over the new offsets)
+      if (nnz > 0 && nnz < (1ull << 31)) {
+        PREP_CK(dalloc(&sort_tmp, nnz));
+        size_t nb2 = 0;
+        if (off64) {
+          const uint64_t* o = (const uint64_t*)new_off;
+          PREP_CK(cub::DeviceSegmentedSort::SortKeys(nullptr, nb2, new_adj, sort_tmp, (int64_t)nnz,
+                                                     (int64_t)n_nz, o, o + 1, s));
+        } else {
+          const uint32_t* o = (const uint32_t*)new_off;
+          PREP_CK(cub::DeviceSegmentedSort::SortKeys(nullptr, nb2, new_adj, sort_tmp, (int64_t)nnz,
+                                                     (int64_t)n_nz, o, o + 1, s));
+        }
+        if (nb2 > tmp_bytes) {
+          PREP_CK(cudaFree(tmp));
+          tmp = nullptr;
+          tmp_bytes = nb2;
+          PREP_CK(cudaMalloc(&tmp, tmp_bytes));
+        }
+        if (off64) {
+          const uint64_t* o = (const uint64_t*)new_off;
+          PREP_CK(cub::DeviceSegmentedSort::SortKeys(tmp, tmp_bytes, new_adj, sort_tmp, (int64_t)nnz,
+                                                     (int64_t)n_nz, o, o + 1, s));
+        } else {
+          const uint32_t* o = (const uint32_t*)new_off;
+          PREP_CK(cub::DeviceSegmentedSort::SortKeys(tmp, tmp_bytes, new_adj, sort_tmp, (int64_t)nnz,
+                                                     (int64_t)n_nz, o, o + 1, s));
+        }
+        std::swap(new_adj, sort_tmp);
+      }
+    }
+    PREP_CK(cudaStreamSynchronize(s));
+  }
+  out->off = new_off;
+  out->adj = new_adj;
+  out->perm = perm;
+  new_off = nullptr;
+  new_adj = nullptr;
+  perm = nullptr;
+done:
+  cudaFree(deg);
+  cudaFree(iota);
+  cudaFree(sdeg);
+  cudaFree(perm);
+  cudaFree(inv);
+  cudaFree(bounds);
+  cudaFree(off64_tmp);
+  cudaFree(chunks);
+  cudaFree(new_off);
+  cudaFree(new_adj);
+  cudaFree(sort_tmp);
+  cudaFree(tmp);
+  return err;
+}
+
+}  // namespace kcb
