@@ -61,8 +61,10 @@ typedef struct kc_options {
   uint32_t max_rounds;     /* 0 = default safety cap */
   uint32_t smem_cache;     /* ids whose estimates are cached in shared memory per
                               round; 0 = default, 0xffffffff = disabled */
-  uint32_t reserved[8];
+  uint32_t reserved[8];    /* reserved[0]: debug flags (KC_DEBUG_*) */
 } kc_options;
+
+#define KC_DEBUG_PHASE_TIMES 1u /* record per-CTA per-round phase timestamps */
 
 /* RunReport (report.hpp:17-23) + work counters and timings. */
 typedef struct kc_stats {
@@ -136,6 +138,13 @@ kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* 
 /* The CUDA stream a handle runs on (cudaStream_t as void*), for callers that
  * want to time kc_solve_device with their own events. */
 void* kc_graph_stream(kc_graph* g);
+
+/* Debug: per-round, per-CTA %globaltimer stamps of the solver phases
+ * (round start, cache filled, HUGE, BIG, WARP, SUB, THREAD done, round end)
+ * from the last solve run with KC_DEBUG_PHASE_TIMES; layout
+ * [256 rounds][grid][8].  *grid receives the CTA count. */
+kc_status kc_debug_phase_times(kc_graph* g, unsigned long long* out, uint64_t cap,
+                               uint32_t* grid);
 
 /* ---- synthetic inputs (BASELINE.json configs; the "kcgen v1" spec) ------ */
 /* Build one of the five configs (1..5) — or a scaled variant — directly on

@@ -15,7 +15,8 @@ from typing import Callable, Iterable, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libkcore_b200.so")
+# KC_LIB_PATH overrides the library (development: A/B builds); default in-tree.
+_LIB_PATH = os.environ.get("KC_LIB_PATH") or os.path.join(_HERE, "libkcore_b200.so")
 
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 
@@ -61,8 +62,9 @@ ABI_SYMBOLS = (
     "kc_graph_upload", "kc_graph_upload_device", "kc_graph_free", "kc_graph_n",
     "kc_graph_nnz", "kc_graph_timings", "kc_solve", "kc_solve_device",
     "kc_solve_observed", "kc_fastk_run", "kc_graph_stream", "kc_gen_config",
-    "kc_csr_dev_free", "kc_csr_dev_download",
+    "kc_csr_dev_free", "kc_csr_dev_download", "kc_debug_phase_times",
 )
+KC_DEBUG_PHASE_TIMES = 1
 
 _lib = None
 
@@ -113,6 +115,9 @@ def load_library():
     L.kc_gen_config.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
                                 C.POINTER(C.POINTER(_CSRDev))]
     L.kc_csr_dev_free.argtypes = [C.POINTER(_CSRDev)]
+    L.kc_debug_phase_times.restype = C.c_int
+    L.kc_debug_phase_times.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64,
+                                       C.POINTER(C.c_uint32)]
     L.kc_csr_dev_download.restype = C.c_int
     L.kc_csr_dev_download.argtypes = [C.POINTER(_CSRDev), C.c_void_p, C.c_void_p]
     _lib = L
@@ -155,6 +160,7 @@ class FastKOptions:
     rule: Rule = Rule.AUTO
     max_rounds: int = 0
     smem_cache: int = 0
+    debug_flags: int = 0
 
     def _c(self) -> _Options:
         o = _Options()
@@ -165,6 +171,7 @@ class FastKOptions:
         o.rule = int(self.rule)
         o.max_rounds = int(self.max_rounds)
         o.smem_cache = int(self.smem_cache) & 0xffffffff
+        o.reserved[0] = int(self.debug_flags)
         return o
 
 
@@ -397,6 +404,14 @@ class GpuGraph:
             raise err[0]
         _check(status, "kc_solve_observed")
         return out[: self.n], st.as_dict()
+
+    def phase_times(self) -> np.ndarray:
+        """[256 rounds, grid, 8] %globaltimer stamps (debug; KC_DEBUG_PHASE_TIMES)."""
+        grid = C.c_uint32()
+        buf = np.zeros(256 * 1024 * 8, dtype=np.uint64)
+        _check(load_library().kc_debug_phase_times(self._h, buf.ctypes.data, buf.size,
+                                                   C.byref(grid)), "kc_debug_phase_times")
+        return buf[: 256 * grid.value * 8].reshape(256, grid.value, 8)
 
     def free(self) -> None:
         if getattr(self, "_h", None):

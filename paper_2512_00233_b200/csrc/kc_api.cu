@@ -76,6 +76,17 @@ __global__ void degree_back_kernel(const OffT* off, const uint32_t* perm, uint32
     out[perm[i]] = i < n_nz ? (uint32_t)(off[i + 1] - off[i]) : 0u;
 }
 
+// Number of set byte flags (observed mode's active_count).
+__global__ void count_flags_kernel(const uint8_t* f, uint32_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    c += f[i] != 0;
+  typedef cub::BlockReduce<unsigned long long, 256> BR;
+  __shared__ typename BR::TempStorage t;
+  const unsigned long long b = BR(t).Sum(c);
+  if (threadIdx.x == 0 && b) atomicAdd(out, b);
+}
+
 // k_max and sum of estimates (n_nz entries).
 __global__ void kstats_kernel(const void* est, bool est16, uint32_t n_nz,
                               unsigned long long* out /* [0]=max, [1]=sum */) {
@@ -114,6 +125,9 @@ struct kc_graph {
   uint32_t max_rounds = 0;
   SolveBuffers sb{};
   uint32_t* d_out = nullptr;      // coreness in caller ids [n]
+  unsigned long long* d_prof = nullptr;  // phase timestamps (debug)
+  unsigned long long* d_count = nullptr; // observed mode: active-flag count
+  uint32_t state_buf = 0;                // est buffer holding the current state
   unsigned long long* d_k = nullptr;
 };
 
@@ -121,31 +135,32 @@ namespace {
 
 void free_solver(kc_graph* g) {
   if (!g->solver_ready) return;
-  cudaFree(g->sb.est);
-  cudaFree(g->sb.queue[0]);
-  cudaFree(g->sb.queue[1]);
-  cudaFree(g->sb.qcnt);
-  cudaFree(g->sb.bm[0]);
-  cudaFree(g->sb.bm[1]);
-  cudaFree(g->sb.drop_u);
-  cudaFree(g->sb.drop_t);
-  cudaFree(g->sb.drop_old);
+  cudaFree(g->sb.est[0]);
+  cudaFree(g->sb.est[1]);
+  cudaFree(g->sb.old);
+  cudaFree(g->sb.flag[0]);
+  cudaFree(g->sb.flag[1]);
+  cudaFree(g->sb.dropped);
   cudaFree(g->sb.ctl);
+  cudaFree(g->sb.anydrop);
   cudaFree(g->sb.stats);
   cudaFree(g->sb.status);
   cudaFree(g->d_out);
   cudaFree(g->d_k);
+  cudaFree(g->d_prof);
+  cudaFree(g->d_count);
+  g->d_prof = nullptr;
+  g->d_count = nullptr;
+  std::memset(&g->sb, 0, sizeof(g->sb));
   g->solver_ready = false;
 }
 
 kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
   (void)max_rounds;
   if (g->solver_ready) return KC_OK;
-  free_solver(g);
   const uint32_t n_nz = g->lay.n_nz;
   const size_t es = g->est16 ? 2 : 4;
-  const size_t n_pad = ((size_t)n_nz + 15) & ~(size_t)15;  // cache fill reads 16 B vectors
-  const size_t words = ((size_t)n_nz + 31) / 32;
+  const size_t n_pad = (((size_t)n_nz + 15) & ~(size_t)15) + 16;  // 16-byte vectors + slack
   SolveBuffers& b = g->sb;
   std::memset(&b, 0, sizeof(b));
   b.off = g->lay.off;
@@ -153,21 +168,24 @@ kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
   b.n_nz = n_nz;
   for (int c = 0; c <= NCLS; ++c) b.cls_begin[c] = g->lay.cls_begin[c];
   g->solver_ready = true;  // so that partial allocations get freed
-  CK(cudaMalloc(&b.est, n_pad * es));
-  CK(cudaMemsetAsync(b.est, 0, n_pad * es, g->stream));
-  CK(cudaMalloc(&b.queue[0], (n_nz ? n_nz : 1) * sizeof(uint32_t)));
-  CK(cudaMalloc(&b.queue[1], (n_nz ? n_nz : 1) * sizeof(uint32_t)));
-  CK(cudaMalloc(&b.qcnt, 2 * NCLS * sizeof(uint32_t)));
-  CK(cudaMalloc(&b.bm[0], (words ? words : 1) * sizeof(uint32_t)));
-  CK(cudaMalloc(&b.bm[1], (words ? words : 1) * sizeof(uint32_t)));
-  CK(cudaMalloc(&b.drop_u, (n_nz ? n_nz : 1) * sizeof(uint32_t)));
-  CK(cudaMalloc(&b.drop_t, (n_nz ? n_nz : 1) * es));
-  CK(cudaMalloc(&b.drop_old, (n_nz ? n_nz : 1) * es));
+  CK(cudaMalloc(&b.est[0], n_pad * es));
+  CK(cudaMalloc(&b.est[1], n_pad * es));
+  CK(cudaMalloc(&b.old, n_pad * es));
+  CK(cudaMalloc(&b.flag[0], n_pad));
+  CK(cudaMalloc(&b.flag[1], n_pad));
+  CK(cudaMalloc(&b.dropped, n_pad));
+  CK(cudaMemsetAsync(b.est[0], 0, n_pad * es, g->stream));
+  CK(cudaMemsetAsync(b.est[1], 0, n_pad * es, g->stream));
+  CK(cudaMemsetAsync(b.flag[0], 0, n_pad, g->stream));
+  CK(cudaMemsetAsync(b.flag[1], 0, n_pad, g->stream));
+  CK(cudaMemsetAsync(b.dropped, 0, n_pad, g->stream));
   CK(cudaMalloc(&b.ctl, 2 * sizeof(Ctl)));
+  CK(cudaMalloc(&b.anydrop, 4 * sizeof(uint32_t)));
   CK(cudaMalloc(&b.stats, (size_t)STAT_SLOTS * sizeof(RoundStat)));
   CK(cudaMalloc(&b.status, 4 * sizeof(uint32_t)));
   CK(cudaMalloc(&g->d_out, (g->n ? g->n : 1) * sizeof(uint32_t)));
   CK(cudaMalloc(&g->d_k, 2 * sizeof(unsigned long long)));
+  CK(cudaMalloc(&g->d_count, sizeof(unsigned long long)));
   g->max_rounds = max_rounds;
   return KC_OK;
 }
@@ -206,6 +224,11 @@ uint32_t cache_entries(const kc_graph* g, const kc_options& o) {
 // Run the solver to convergence (or one round when `one_round`), leaving the
 // estimates on the device.  Fills the counters of `st`.
 kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_t r_end) {
+  if ((o.reserved[0] & KC_DEBUG_PHASE_TIMES) && !g->d_prof) {
+    CK(cudaMalloc(&g->d_prof, (size_t)PROF_ROUNDS * g->num_sms * PROF_PHASES * 8));
+    CK(cudaMemsetAsync(g->d_prof, 0, (size_t)PROF_ROUNDS * g->num_sms * PROF_PHASES * 8, g->stream));
+  }
+  g->sb.prof = (o.reserved[0] & KC_DEBUG_PHASE_TIMES) ? g->d_prof : nullptr;
   SolveConfig c{};
   c.rule = map_rule(o);
   c.cache_n = cache_entries(g, o);
@@ -222,6 +245,7 @@ kc_status collect(kc_graph* g, const kc_options& o, kc_stats* st, bool* converge
   CK(cudaStreamSynchronize(g->stream));
   const uint32_t rounds = status[0];
   *converged = status[1] != 0;
+  g->state_buf = status[3] & 1;
   if (!st) return KC_OK;
   const uint32_t slots = rounds < STAT_SLOTS ? rounds : STAT_SLOTS;
   std::vector<RoundStat> rs(slots);
@@ -249,7 +273,8 @@ kc_status kstats(kc_graph* g, kc_stats* st) {
   unsigned long long k[2] = {0, 0};
   CK(cudaMemsetAsync(g->d_k, 0, 2 * sizeof(unsigned long long), g->stream));
   if (g->lay.n_nz) {
-    kstats_kernel<<<g->num_sms * 2, 256, 0, g->stream>>>(g->sb.est, g->est16, g->lay.n_nz, g->d_k);
+    kstats_kernel<<<g->num_sms * 2, 256, 0, g->stream>>>(g->sb.est[g->state_buf], g->est16,
+                                                        g->lay.n_nz, g->d_k);
     CK(cudaGetLastError());
   }
   CK(cudaMemcpyAsync(k, g->d_k, sizeof(k), cudaMemcpyDeviceToHost, g->stream));
@@ -262,7 +287,8 @@ kc_status kstats(kc_graph* g, kc_stats* st) {
 
 kc_status permute_back(kc_graph* g) {
   if (!g->n) return KC_OK;
-  permute_back_kernel<<<g->num_sms * 4, 256, 0, g->stream>>>(g->sb.est, g->est16, g->lay.perm,
+  permute_back_kernel<<<g->num_sms * 4, 256, 0, g->stream>>>(g->sb.est[g->state_buf], g->est16,
+                                                             g->lay.perm,
                                                              g->n, g->lay.n_nz, g->d_out);
   CK(cudaGetLastError());
   return KC_OK;
@@ -335,7 +361,7 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, kc_g
   if (e != cudaSuccess) return bail(cuda_fail(e, "layout"));
   cudaEventElapsedTime(&g->t_upload, g->ev[0], g->ev[1]);
   cudaEventElapsedTime(&g->t_prep, g->ev[1], g->ev[2]);
-  g->est16 = g->lay.h_graph < 65535u;
+  g->est16 = g->lay.h_graph < EST16_LIMIT;
   *out = g;
   return KC_OK;
 }
@@ -517,14 +543,19 @@ kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn 
     if (s != KC_OK) return s;
     s = collect(g, o, nullptr, &conv);
     if (s != KC_OK) return s;
-    RoundStat rs;
-    CK(cudaMemcpy(&rs, g->sb.stats + (r < STAT_SLOTS - 1 ? r : STAT_SLOTS - 1), sizeof(rs),
-                  cudaMemcpyDeviceToHost));
+    unsigned long long active = 0;
+    if (!conv) {  // flags collected for round r+1 (the reference's active_count)
+      CK(cudaMemsetAsync(g->d_count, 0, sizeof(unsigned long long), g->stream));
+      count_flags_kernel<<<g->num_sms * 2, 256, 0, g->stream>>>(g->sb.flag[(r + 1) & 1],
+                                                                g->lay.n_nz, g->d_count);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(&active, g->d_count, sizeof(active), cudaMemcpyDeviceToHost, g->stream));
+    }
     s = permute_back(g);
     if (s != KC_OK) return s;
     CK(cudaMemcpyAsync(snap.data(), g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
     CK(cudaStreamSynchronize(g->stream));
-    if (fn && fn(user, (uint64_t)r + 1, snap.data(), g->n, conv ? 0 : rs.active_after))
+    if (fn && fn(user, (uint64_t)r + 1, snap.data(), g->n, active))
       return fail(KC_ERR_CALLBACK, "inspector");
   }
   if (!conv) return fail(KC_ERR_NOT_CONVERGED, "round cap reached");
@@ -533,6 +564,16 @@ kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn 
   s = kstats(g, st);
   if (s != KC_OK) return s;
   std::memcpy(coreness, snap.data(), g->n * sizeof(uint32_t));
+  return KC_OK;
+}
+
+kc_status kc_debug_phase_times(kc_graph* g, unsigned long long* out, uint64_t cap,
+                               uint32_t* grid) {
+  if (!g || !out || !grid) return fail(KC_ERR_INVALID_ARGUMENT, "null argument");
+  *grid = (uint32_t)g->num_sms;
+  if (!g->d_prof) return fail(KC_ERR_INVALID_ARGUMENT, "no phase times recorded");
+  const uint64_t total = (uint64_t)PROF_ROUNDS * g->num_sms * PROF_PHASES;
+  CK(cudaMemcpy(out, g->d_prof, (cap < total ? cap : total) * 8, cudaMemcpyDeviceToHost));
   return KC_OK;
 }
 

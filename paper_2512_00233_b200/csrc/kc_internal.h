@@ -9,48 +9,56 @@ namespace kcb {
 
 // Degree classes.  Vertex ids are relabelled by descending degree at upload
 // (kc_prep.cu), so class c is the id range [cls_begin[c], cls_begin[c+1]).
-enum Cls : int { C_HUGE = 0, C_BLOCK = 1, C_WARP = 2, C_SUB = 3, C_THREAD = 4, NCLS = 5 };
-constexpr uint32_t DEG_THREAD_MAX = 8;     // one thread per vertex, values in registers
-constexpr uint32_t DEG_SUB_MAX = 64;       // 8-lane tile per vertex, 8 values per lane
-constexpr uint32_t DEG_WARP_MAX = 1024;    // warp per vertex, 32 values per lane
-constexpr uint32_t DEG_BLOCK_MAX = 32768;  // CTA per vertex, windowed histogram
-                                           // (> DEG_BLOCK_MAX: CTA per vertex, same code)
-constexpr int SOLVE_THREADS = 1024;
-constexpr int HIST_BINS = 4096;            // windowed histogram, 16 KB of shared memory
+enum Cls : int { C_HUGE = 0, C_BIG = 1, C_WARP = 2, C_SUB = 3, C_THREAD = 4, NCLS = 5 };
+constexpr uint32_t DEG_THREAD_MAX = 8;   // THREAD: one thread per vertex, values in registers
+constexpr uint32_t DEG_SUB_MAX = 64;     // SUB:    8-lane tile per vertex, 8 values per lane
+constexpr uint32_t DEG_WARP_MAX = 1020;  // WARP:   warp per vertex, 32 values per lane
+                                         //         (1020: a misaligned row still fits
+                                         //          8 aligned 128-bit loads per lane)
+constexpr uint32_t DEG_BIG_MAX = 8192;   // BIG:    warp per vertex, streamed, warp histogram
+                                         // HUGE:   CTA per vertex, streamed, CTA histogram
+constexpr int SOLVE_THREADS = 512;
+constexpr int HIST_BINS = 4096;          // CTA windowed histogram (16 KB of shared memory)
+constexpr int WARP_BINS = 256;           // per-warp windowed histogram (32 x 1 KB)
+constexpr uint32_t EST16_LIMIT = 32768;  // 16-bit estimates need H < 2^15 (packed compares)
+constexpr uint32_t ADJ_PAD = 8;          // neighbours allocated with 8 spare entries
+                                         // (aligned 128-bit loads may read past a row)
 
 // Activation rules (see include/kcore_b200.h kc_rule and SURVEY.md §7.3).
 enum Rule : int { R_REF_EXT = 0, R_REF_PLAIN = 1, R_SNAP_EXT = 2, R_SNAP_PLAIN = 3 };
 
-struct Ctl {                 // per round parity: work-grab cursors + drop count
-  uint32_t grab[NCLS];
-  uint32_t ndrops;
-  uint32_t pad[2];
+struct Ctl {                 // per round parity: work-grab cursors
+  uint32_t grab[NCLS + 2];   // [NCLS]: REF notify scan, [NCLS+1]: spare
+  uint32_t pad;
 };
 
 constexpr uint32_t STAT_SLOTS = 4096;  // rounds >= STAT_SLOTS-1 share the last slot
 
 struct RoundStat {           // per round, accumulated with atomics
-  unsigned long long evals, escan, drops, fires, frontier, active_after, tail, pad;
+  unsigned long long evals, escan, drops, fires, pad0, pad1, pad2, pad3;
 };
 
 struct SolveBuffers {
   // layout (owned by kc_graph)
   const void* off;           // uint32 or uint64, n_nz + 1 (relabelled ids)
-  const uint32_t* adj;       // relabelled neighbours
-  void* est;                 // uint16 or uint32 [n_nz]
+  const uint32_t* adj;       // relabelled neighbours (+ ADJ_PAD)
   uint32_t n_nz;
   uint32_t cls_begin[NCLS + 1];
-  // frontier state
-  uint32_t* queue[2];        // [n_nz] each, class c segment at cls_begin[c]
-  uint32_t* qcnt;            // [2][NCLS]
-  uint32_t* bm[2];           // dedup bitmaps, (n_nz + 31) / 32 words
-  uint32_t* drop_u;          // [n_nz]
-  void* drop_t;              // EstT [n_nz]
-  void* drop_old;            // EstT [n_nz]
+  // estimates: snapshot rule double-buffers est[r & 1] -> est[(r + 1) & 1];
+  // reference rule keeps est[0] and uses est[1] for the round's new values
+  void* est[2];              // uint16 or uint32 [n_pad] each
+  void* old;                 // EstT [n_pad]: reference rule, value before the drop
+  uint8_t* flag[2];          // frontier byte flags, flag[r & 1] read + cleared in round r
+  uint8_t* dropped;          // reference rule: dropped-this-round marks
   Ctl* ctl;                  // [2]
+  uint32_t* anydrop;         // [3] "some estimate dropped in round r" (r % 3)
   RoundStat* stats;          // [STAT_SLOTS]
-  uint32_t* status;          // [0] rounds completed, [1] converged, [2] tail rounds
+  uint32_t* status;          // [0] rounds completed, [1] converged, [2] tail rounds,
+                             // [3] est buffer holding the current state
+  unsigned long long* prof;  // optional phase timestamps [PROF_ROUNDS][grid][PROF_PHASES]
 };
+constexpr uint32_t PROF_ROUNDS = 256;
+constexpr uint32_t PROF_PHASES = 8;
 
 struct SolveConfig {
   int rule;

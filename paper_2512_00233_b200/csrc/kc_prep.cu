@@ -34,8 +34,8 @@ __global__ void inverse_kernel(const uint32_t* __restrict__ perm, uint32_t n,
 }
 
 // Boundaries on the descending degree sequence: out[0] = H (h-index of the
-// degree sequence), out[1..4] = #vertices with degree > {32768, 1024, 64, 8},
-// out[5] = #vertices with degree > 0 (n_nz).
+// degree sequence), out[1..4] = #vertices with degree > {8192, 1024, 64, 8},
+// out[5] = #vertices with degree > 0 (n_nz).  Thresholds: kc_internal.h.
 __global__ void bounds_kernel(const uint32_t* __restrict__ sdeg, uint32_t n, uint32_t* out) {
   const uint32_t k = threadIdx.x;
   if (k > 5) return;
@@ -48,7 +48,7 @@ __global__ void bounds_kernel(const uint32_t* __restrict__ sdeg, uint32_t n, uin
     out[0] = lo;
     return;
   }
-  const uint32_t thr[6] = {0, DEG_BLOCK_MAX, DEG_WARP_MAX, DEG_SUB_MAX, DEG_THREAD_MAX, 0};
+  const uint32_t thr[6] = {0, DEG_BIG_MAX, DEG_WARP_MAX, DEG_SUB_MAX, DEG_THREAD_MAX, 0};
   const uint32_t t = thr[k];
   uint32_t lo = 0, hi = n;  // count of sdeg[i] > t (prefix, sdeg descending)
   while (lo < hi) {
@@ -190,7 +190,8 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
       narrow_offsets_kernel<uint32_t><<<G, B, 0, s>>>(off64_tmp, n_nz + 1, (uint32_t*)new_off);
       PREP_CK(cudaGetLastError());
     }
-    PREP_CK(dalloc(&new_adj, nnz));
+    PREP_CK(dalloc(&new_adj, nnz + ADJ_PAD));
+    PREP_CK(cudaMemsetAsync(new_adj + nnz, 0, ADJ_PAD * sizeof(uint32_t), s));
     PREP_CK(dalloc(&chunks, (size_t)n_nz + 1));
     if (n_nz) {
       if (off64)
@@ -221,7 +222,8 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
       PREP_CK(cudaGetLastError());
       // sort each row ascending (segmented sort over the new offsets)
       if (nnz > 0 && nnz < (1ull << 31)) {
-        PREP_CK(dalloc(&sort_tmp, nnz));
+        PREP_CK(dalloc(&sort_tmp, nnz + ADJ_PAD));
+        PREP_CK(cudaMemsetAsync(sort_tmp + nnz, 0, ADJ_PAD * sizeof(uint32_t), s));
         size_t nb2 = 0;
         if (off64) {
           const uint64_t* o = (const uint64_t*)new_off;

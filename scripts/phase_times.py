@@ -1,0 +1,35 @@
+"""Per-round phase timing of the persistent solver (debug instrumentation)."""
+import argparse, sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_2512_00233_b200 as K
+from paper_2512_00233_b200.api import KC_DEBUG_PHASE_TIMES
+from bench import CONFIGS
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=3)
+ap.add_argument("--scale", type=int, default=0)
+ap.add_argument("--rule", type=int, default=2)
+ap.add_argument("--cache", type=int, default=0)
+a = ap.parse_args()
+desc, (p0, p1, p2), seed = CONFIGS[a.config]
+if a.scale: p0 = a.scale
+d = K.gen_config(a.config, p0, p1, p2, seed=seed)
+g = K.GpuGraph(d)
+o = K.FastKOptions(rule=K.Rule(a.rule), smem_cache=a.cache)
+g.solve(o)
+core, st = g.solve(o)
+print("plain solve ms", st["t_solve_ms"], "iters", st["iterations"])
+o.debug_flags = KC_DEBUG_PHASE_TIMES
+core, st = g.solve(o)
+print("instrumented solve ms", st["t_solve_ms"])
+pt = g.phase_times().astype(np.int64)
+R = min(st["iterations"], 256)
+names = ["cache", "huge", "big", "warp", "sub", "thread", "sync+apply"]
+t0 = pt[0, :, 0].min()
+print("round  start_us  " + " ".join(f"{n:>10s}" for n in names) + "   (max over CTAs, us)")
+tot = np.zeros(7)
+for r in range(R):
+    d = np.diff(pt[r], axis=1) / 1e3  # per CTA per phase
+    mx = d.max(axis=0); tot += mx
+    print(f"{r:5d} {(pt[r,:,0].min()-t0)/1e3:9.1f}  " + " ".join(f"{x:10.1f}" for x in mx))
+print("sum of max:", " ".join(f"{n}={x:.0f}" for n, x in zip(names, tot)))

@@ -1,0 +1,22 @@
+"""Profiling driver: build a config on the GPU, lay it out, solve it `--reps`
+times (the first is warm-up).  Used under ncu with -k regex:rounds_kernel."""
+import argparse, sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_2512_00233_b200 as K
+from bench import CONFIGS
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=3)
+ap.add_argument("--scale", type=int, default=0)
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--rule", type=int, default=2)
+ap.add_argument("--cache", type=int, default=0)
+a = ap.parse_args()
+desc, (p0, p1, p2), seed = CONFIGS[a.config]
+if a.scale: p0 = a.scale
+d = K.gen_config(a.config, p0, p1, p2, seed=seed)
+g = K.GpuGraph(d)
+for i in range(a.reps):
+    core, st = g.solve(K.FastKOptions(rule=K.Rule(a.rule), smem_cache=a.cache))
+    print(i, {k: st[k] for k in ("iterations", "e_scan", "v_eval", "t_solve_ms", "k_max")}, flush=True)
