@@ -38,17 +38,21 @@ typedef enum kc_status {
   KC_ERR_CALLBACK = 6          /* an inspector callback asked to stop */
 } kc_status;
 
-/* Activation rule.  Every rule reaches the same unique fixed
- * point; they differ in how many vertices are re-evaluated per round. */
+/* Which vertices a round re-evaluates.  Every rule follows
+ * the same Jacobi estimate trajectory (shadow_run, tests/test_fastk.cpp:41-92)
+ * and reaches the same unique fixed point. */
 typedef enum kc_rule {
-  /* extended_notify judged on SETTLED estimates after the round's updates —
-   * exactly fastk_run's notify phase (fastk.cpp:156-163).  With
-   * hybrid_tail = 0 the RunReport counters equal the reference's. */
+  /* fastk_run's rule: droppers notify neighbours with extended_notify judged
+   * on SETTLED estimates (fastk.cpp:156-163); notified vertices are
+   * re-evaluated.  With hybrid_tail = 0 the RunReport counters equal the
+   * reference's. */
   KC_RULE_REFERENCE = 0,
-  /* every dropper re-activates itself, neighbours judged with the extended
-   * rule on the round's snapshot, in the same pass (no settled re-scan). */
-  KC_RULE_SNAPSHOT = 1,
-  KC_RULE_AUTO = 2 /* the fastest safe rule (currently KC_RULE_SNAPSHOT) */
+  /* support counters: cnt[v] = #{w in N(v) : est_w >= est_v}; a drop of u
+   * across est_w (the extended rule on settled values) decrements cnt[w], and
+   * w is re-evaluated iff cnt[w] < est_w — i.e. only vertices that WILL drop
+   * are evaluated.  messages_sent counts decrements. */
+  KC_RULE_COUNTING = 1,
+  KC_RULE_AUTO = 2 /* the fastest rule (currently KC_RULE_COUNTING) */
 } kc_rule;
 
 /* FastKOptions (include/kcore/fastk.hpp:12-22) plus GPU knobs. */
@@ -116,6 +120,12 @@ kc_status kc_graph_upload(const kc_csr_view* csr, int device, kc_graph** out);
 /* Same, but `csr` points at DEVICE memory on `device` (e.g. a graph built by
  * kc_gen_*); the source buffers are only read. */
 kc_status kc_graph_upload_device(const kc_csr_view* csr, int device, kc_graph** out);
+/* Upload with layout flags (KC_UPLOAD_*); `on_device` selects the pointer
+ * space of `csr` as above. */
+#define KC_UPLOAD_FORCE_OFF64 1u /* 64-bit device offsets even when nnz < 2^32 */
+#define KC_UPLOAD_FORCE_EST32 2u /* 32-bit estimates even when H < 2^15 */
+kc_status kc_graph_upload_ex(const kc_csr_view* csr, int device, int on_device, uint32_t flags,
+                             kc_graph** out);
 void kc_graph_free(kc_graph* g);
 uint32_t kc_graph_n(const kc_graph* g);
 uint64_t kc_graph_nnz(const kc_graph* g);

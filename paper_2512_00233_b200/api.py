@@ -62,9 +62,11 @@ ABI_SYMBOLS = (
     "kc_graph_upload", "kc_graph_upload_device", "kc_graph_free", "kc_graph_n",
     "kc_graph_nnz", "kc_graph_timings", "kc_solve", "kc_solve_device",
     "kc_solve_observed", "kc_fastk_run", "kc_graph_stream", "kc_gen_config",
-    "kc_csr_dev_free", "kc_csr_dev_download", "kc_debug_phase_times",
+    "kc_csr_dev_free", "kc_csr_dev_download", "kc_debug_phase_times", "kc_graph_upload_ex",
 )
 KC_DEBUG_PHASE_TIMES = 1
+KC_UPLOAD_FORCE_OFF64 = 1
+KC_UPLOAD_FORCE_EST32 = 2
 
 _lib = None
 
@@ -92,6 +94,9 @@ def load_library():
     L.kc_graph_upload.argtypes = [C.POINTER(_CSRView), C.c_int, C.POINTER(C.c_void_p)]
     L.kc_graph_upload_device.restype = C.c_int
     L.kc_graph_upload_device.argtypes = [C.POINTER(_CSRView), C.c_int, C.POINTER(C.c_void_p)]
+    L.kc_graph_upload_ex.restype = C.c_int
+    L.kc_graph_upload_ex.argtypes = [C.POINTER(_CSRView), C.c_int, C.c_int, C.c_uint32,
+                                     C.POINTER(C.c_void_p)]
     L.kc_graph_free.argtypes = [C.c_void_p]
     L.kc_graph_n.restype = C.c_uint32
     L.kc_graph_n.argtypes = [C.c_void_p]
@@ -145,8 +150,8 @@ def _check(status: int, where: str) -> None:
 # Reference types
 # --------------------------------------------------------------------------
 class Rule(enum.IntEnum):
-    REFERENCE = 0   # extended rule on settled values (fastk.cpp:156-163)
-    SNAPSHOT = 1    # self-activation + extended rule on the snapshot, one pass
+    REFERENCE = 0   # notify on settled values, re-evaluate notified (fastk.cpp:156-163)
+    COUNTING = 1    # support counters: only vertices that will drop are evaluated
     AUTO = 2
 
 
@@ -342,17 +347,18 @@ def gen_config(cfg: int, p0: int, p1: int = 0, p2: int = 0, seed: int = 1,
 class GpuGraph:
     """An uploaded, laid-out graph handle (kc_graph)."""
 
-    def __init__(self, g, device: int = 0):
+    def __init__(self, g, device: int = 0, flags: int = 0):
         L = load_library()
         self._h = C.c_void_p()
         if isinstance(g, DeviceCSR):
             v = g.view()
-            _check(L.kc_graph_upload_device(C.byref(v), device, C.byref(self._h)),
-                   "kc_graph_upload_device")
+            _check(L.kc_graph_upload_ex(C.byref(v), device, 1, flags, C.byref(self._h)),
+                   "kc_graph_upload_ex")
         else:
             self._keep = g
             v = g._view()
-            _check(L.kc_graph_upload(C.byref(v), device, C.byref(self._h)), "kc_graph_upload")
+            _check(L.kc_graph_upload_ex(C.byref(v), device, 0, flags, C.byref(self._h)),
+                   "kc_graph_upload_ex")
         self.n = L.kc_graph_n(self._h)
         self.nnz = L.kc_graph_nnz(self._h)
 

@@ -137,10 +137,10 @@ void free_solver(kc_graph* g) {
   if (!g->solver_ready) return;
   cudaFree(g->sb.est[0]);
   cudaFree(g->sb.est[1]);
-  cudaFree(g->sb.old);
+  cudaFree(g->sb.cnt);
+  cudaFree(g->sb.queue);
   cudaFree(g->sb.flag[0]);
   cudaFree(g->sb.flag[1]);
-  cudaFree(g->sb.dropped);
   cudaFree(g->sb.ctl);
   cudaFree(g->sb.anydrop);
   cudaFree(g->sb.stats);
@@ -170,15 +170,14 @@ kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
   g->solver_ready = true;  // so that partial allocations get freed
   CK(cudaMalloc(&b.est[0], n_pad * es));
   CK(cudaMalloc(&b.est[1], n_pad * es));
-  CK(cudaMalloc(&b.old, n_pad * es));
+  CK(cudaMalloc(&b.cnt, n_pad * sizeof(uint32_t)));
+  CK(cudaMalloc(&b.queue, n_pad * sizeof(uint32_t)));
   CK(cudaMalloc(&b.flag[0], n_pad));
   CK(cudaMalloc(&b.flag[1], n_pad));
-  CK(cudaMalloc(&b.dropped, n_pad));
   CK(cudaMemsetAsync(b.est[0], 0, n_pad * es, g->stream));
   CK(cudaMemsetAsync(b.est[1], 0, n_pad * es, g->stream));
   CK(cudaMemsetAsync(b.flag[0], 0, n_pad, g->stream));
   CK(cudaMemsetAsync(b.flag[1], 0, n_pad, g->stream));
-  CK(cudaMemsetAsync(b.dropped, 0, n_pad, g->stream));
   CK(cudaMalloc(&b.ctl, 2 * sizeof(Ctl)));
   CK(cudaMalloc(&b.anydrop, 4 * sizeof(uint32_t)));
   CK(cudaMalloc(&b.stats, (size_t)STAT_SLOTS * sizeof(RoundStat)));
@@ -193,7 +192,7 @@ kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
 int map_rule(const kc_options& o) {
   const bool ref = o.rule == KC_RULE_REFERENCE;
   if (ref) return o.extended_notify ? R_REF_EXT : R_REF_PLAIN;
-  return o.extended_notify ? R_SNAP_EXT : R_SNAP_PLAIN;
+  return R_COUNT;  // exact activation: extended_notify cannot change it
 }
 
 kc_status validate(const kc_options* opt, kc_options* o) {
@@ -202,7 +201,7 @@ kc_status validate(const kc_options* opt, kc_options* o) {
   if (o->threads == 0) return fail(KC_ERR_INVALID_ARGUMENT, "fastk: threads must be >= 1");
   if (o->batch == 0) return fail(KC_ERR_INVALID_ARGUMENT, "fastk: batch must be >= 1");
   if (o->rule < 0 || o->rule > KC_RULE_AUTO) return fail(KC_ERR_INVALID_ARGUMENT, "unknown rule");
-  if (o->rule == KC_RULE_AUTO) o->rule = KC_RULE_SNAPSHOT;
+  if (o->rule == KC_RULE_AUTO) o->rule = KC_RULE_COUNTING;
   // Every round with a drop lowers sum(est) by >= 1, so the loop terminates;
   // 0 means no cap (paths need ~n/2 Jacobi rounds).
   if (o->max_rounds == 0) o->max_rounds = 0xffffffffu;
@@ -231,6 +230,7 @@ kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_
   g->sb.prof = (o.reserved[0] & KC_DEBUG_PHASE_TIMES) ? g->d_prof : nullptr;
   SolveConfig c{};
   c.rule = map_rule(o);
+  c.clamp_drop = g->lay.max_degree > g->lay.h_graph ? 1u : 0u;
   c.cache_n = cache_entries(g, o);
   c.max_rounds = o.max_rounds;
   c.tail_threshold = 0;
@@ -294,7 +294,8 @@ kc_status permute_back(kc_graph* g) {
   return KC_OK;
 }
 
-kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, kc_graph** out) {
+kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint32_t flags,
+                        kc_graph** out) {
   if (!out) return fail(KC_ERR_INVALID_ARGUMENT, "out is null");
   *out = nullptr;
   if (!csr) return fail(KC_ERR_INVALID_ARGUMENT, "csr view is null");
@@ -351,7 +352,8 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, kc_g
     cudaEventRecord(g->ev[0], g->stream);
     cudaEventRecord(g->ev[1], g->stream);
   }
-  e = prep_layout(d_off, d_adj, g->n, g->nnz, false, g->stream, &g->lay);
+  e = prep_layout(d_off, d_adj, g->n, g->nnz, (flags & KC_UPLOAD_FORCE_OFF64) != 0, g->stream,
+                  &g->lay);
   cudaEventRecord(g->ev[2], g->stream);
   cudaStreamSynchronize(g->stream);
   if (!on_device) {
@@ -361,7 +363,7 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, kc_g
   if (e != cudaSuccess) return bail(cuda_fail(e, "layout"));
   cudaEventElapsedTime(&g->t_upload, g->ev[0], g->ev[1]);
   cudaEventElapsedTime(&g->t_prep, g->ev[1], g->ev[2]);
-  g->est16 = g->lay.h_graph < EST16_LIMIT;
+  g->est16 = g->lay.h_graph < EST16_LIMIT && !(flags & KC_UPLOAD_FORCE_EST32);
   *out = g;
   return KC_OK;
 }
@@ -401,12 +403,20 @@ void kc_default_options(kc_options* o) {
 
 kc_status kc_graph_upload(const kc_csr_view* csr, int device, kc_graph** out) {
   g_last_error.clear();
-  return upload_common(csr, device, false, out);
+  return upload_common(csr, device, false, 0u, out);
 }
 
 kc_status kc_graph_upload_device(const kc_csr_view* csr, int device, kc_graph** out) {
   g_last_error.clear();
-  return upload_common(csr, device, true, out);
+  return upload_common(csr, device, true, 0u, out);
+}
+
+kc_status kc_graph_upload_ex(const kc_csr_view* csr, int device, int on_device, uint32_t flags,
+                             kc_graph** out) {
+  g_last_error.clear();
+  if (flags & ~(KC_UPLOAD_FORCE_OFF64 | KC_UPLOAD_FORCE_EST32))
+    return fail(KC_ERR_INVALID_ARGUMENT, "unknown upload flags");
+  return upload_common(csr, device, on_device != 0, flags, out);
 }
 
 void kc_graph_free(kc_graph* g) {

@@ -17,7 +17,10 @@ constexpr uint32_t DEG_WARP_MAX = 1020;  // WARP:   warp per vertex, 32 values p
                                          //          8 aligned 128-bit loads per lane)
 constexpr uint32_t DEG_BIG_MAX = 8192;   // BIG:    warp per vertex, streamed, warp histogram
                                          // HUGE:   CTA per vertex, streamed, CTA histogram
-constexpr int SOLVE_THREADS = 512;
+#ifndef KC_SOLVE_THREADS
+#define KC_SOLVE_THREADS 512
+#endif
+constexpr int SOLVE_THREADS = KC_SOLVE_THREADS;
 constexpr int HIST_BINS = 4096;          // CTA windowed histogram (16 KB of shared memory)
 constexpr int WARP_BINS = 256;           // per-warp windowed histogram (32 x 1 KB)
 constexpr uint32_t EST16_LIMIT = 32768;  // 16-bit estimates need H < 2^15 (packed compares)
@@ -25,11 +28,15 @@ constexpr uint32_t ADJ_PAD = 8;          // neighbours allocated with 8 spare en
                                          // (aligned 128-bit loads may read past a row)
 
 // Activation rules (see include/kcore_b200.h kc_rule and SURVEY.md §7.3).
-enum Rule : int { R_REF_EXT = 0, R_REF_PLAIN = 1, R_SNAP_EXT = 2, R_SNAP_PLAIN = 3 };
+//   R_REF_*   notified vertices are re-evaluated (fastk.cpp:156-163), flags
+//   R_COUNT   support counters: only vertices that will drop are evaluated
+enum Rule : int { R_REF_EXT = 0, R_REF_PLAIN = 1, R_COUNT = 2 };
 
-struct Ctl {                 // per round parity: work-grab cursors
-  uint32_t grab[NCLS + 2];   // [NCLS]: REF notify scan, [NCLS+1]: spare
-  uint32_t pad;
+struct Ctl {                 // per round parity
+  uint32_t grab[NCLS];       // evaluate phase cursors, per class
+  uint32_t grab2[NCLS];      // notify phase cursors, per class
+  uint32_t qcnt[NCLS];       // active vertices of each class (compacted queue)
+  uint32_t pad[1];
 };
 
 constexpr uint32_t STAT_SLOTS = 4096;  // rounds >= STAT_SLOTS-1 share the last slot
@@ -44,12 +51,13 @@ struct SolveBuffers {
   const uint32_t* adj;       // relabelled neighbours (+ ADJ_PAD)
   uint32_t n_nz;
   uint32_t cls_begin[NCLS + 1];
-  // estimates: snapshot rule double-buffers est[r & 1] -> est[(r + 1) & 1];
-  // reference rule keeps est[0] and uses est[1] for the round's new values
+  // est[0] = E, the round's snapshot; est[1] = N, the settled values (N == E
+  // at every round start; the evaluate phase lowers N, the notify phase
+  // copies droppers' N back into E)
   void* est[2];              // uint16 or uint32 [n_pad] each
-  void* old;                 // EstT [n_pad]: reference rule, value before the drop
-  uint8_t* flag[2];          // frontier byte flags, flag[r & 1] read + cleared in round r
-  uint8_t* dropped;          // reference rule: dropped-this-round marks
+  uint32_t* cnt;             // R_COUNT: #neighbours w with est_w >= est_v [n_pad]
+  uint8_t* flag[2];          // frontier byte flags; flag[r & 1] = round r's active set
+  uint32_t* queue;           // [n_pad] round r's active ids, class c segment at cls_begin[c]
   Ctl* ctl;                  // [2]
   uint32_t* anydrop;         // [3] "some estimate dropped in round r" (r % 3)
   RoundStat* stats;          // [STAT_SLOTS]
@@ -62,6 +70,7 @@ constexpr uint32_t PROF_PHASES = 8;
 
 struct SolveConfig {
   int rule;
+  uint32_t clamp_drop;       // max degree > H (round 0 changed in the reference)
   uint32_t cache_n;          // ids cached in shared memory
   uint32_t max_rounds;
   uint32_t tail_threshold;   // frontier size below which one CTA finishes (0 = off)
@@ -85,6 +94,7 @@ struct PrepOut {
   uint32_t* perm;   // [n] new id -> caller id
   uint32_t n_nz;    // non-isolated vertices (ids [0, n_nz))
   uint32_t h_graph; // h-index of the degree sequence
+  uint32_t max_degree;
   uint32_t cls_begin[NCLS + 1];
   bool off64;
 };

@@ -35,9 +35,10 @@ __global__ void inverse_kernel(const uint32_t* __restrict__ perm, uint32_t n,
 
 // Boundaries on the descending degree sequence: out[0] = H (h-index of the
 // degree sequence), out[1..4] = #vertices with degree > {8192, 1024, 64, 8},
-// out[5] = #vertices with degree > 0 (n_nz).  Thresholds: kc_internal.h.
+// out[5] = #vertices with degree > 0 (n_nz), out[6] = maximum degree.  Thresholds: kc_internal.h.
 __global__ void bounds_kernel(const uint32_t* __restrict__ sdeg, uint32_t n, uint32_t* out) {
   const uint32_t k = threadIdx.x;
+  if (k == 6) out[6] = n ? sdeg[0] : 0u;  // maximum degree
   if (k > 5) return;
   if (k == 0) {  // largest h with sdeg[h-1] >= h
     uint32_t lo = 0, hi = n;  // answer in [lo, hi]
@@ -132,7 +133,7 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
   uint32_t* sort_tmp = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0, need = 0;
-  uint32_t hb[6] = {0, 0, 0, 0, 0, 0};
+  uint32_t hb[7] = {0, 0, 0, 0, 0, 0, 0};
   const bool off64 = force_off64 || nnz >= (1ull << 32);
   const int G = 148 * 8, B = 256;
   out->off = nullptr;
@@ -159,6 +160,7 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
   PREP_CK(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, s));
   PREP_CK(cudaStreamSynchronize(s));
   out->h_graph = hb[0];
+  out->max_degree = hb[6];
   out->n_nz = hb[5];
   out->cls_begin[0] = 0;
   for (int c = 1; c <= 4; ++c) out->cls_begin[c] = hb[c];

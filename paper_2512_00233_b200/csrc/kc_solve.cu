@@ -7,25 +7,32 @@
 //   compute_index_over   include/kcore/kernel.hpp:27-42 — capped h-index
 //   should_notify        include/kcore/fastk.hpp:25-27  — extended activation rule
 //
-// State: the frontier is a byte flag per vertex (flag[r&1] is read and
-// cleared in round r, flag[(r+1)&1] collects activations with plain stores —
-// no atomics, no queue appends); vertices are relabelled by descending degree
-// so the degree classes (kc_internal.h) are id ranges that workers scan in
-// chunks.
+// State.  E (est[0]) is the round's snapshot, N (est[1]) the settled values;
+// N == E at every round start.  The frontier is a byte flag per vertex:
+// flag[r&1] is round r's active set, flag[(r+1)&1] collects the next one with
+// plain stores.  Vertices are relabelled by descending degree at upload, so
+// the degree classes (kc_internal.h) are id ranges that workers scan in
+// chunks, and est[0, cache_n) — the most-gathered estimates — is cached in
+// every CTA's shared memory.
 //
-// Snapshot rule (default), one grid barrier per round:
-//   est[r&1] is the round's snapshot (Jacobi, like the reference's process
-//   phase reading est while updates are buffered, fastk.cpp:128-153); every
-//   evaluated vertex writes its new value to est[(r+1)&1].  Every dropper
-//   re-activates itself, so a vertex not evaluated in round r did not change
-//   in round r-1 and its est[(r+1)&1] entry (written two rounds ago) is
-//   already current: no drop list, no apply pass.  Neighbours are activated
-//   with the extended rule judged on the snapshot (SURVEY §7.3 rule C).
-// Reference rule (exact RunReport counters), three barriers per round:
-//   evaluate (droppers record new/old value), apply (fastk.cpp:153), notify
-//   on settled values (fastk.cpp:156-163).
-// Per round every CTA first caches est[0, cache_n) — the highest-degree ids —
-// in shared memory.  No host synchronisation happens between rounds.
+// One round = two grid barriers:
+//   EVALUATE  every active u computes t = capped h-index of E over its row
+//             (the reference's process phase on a frozen snapshot,
+//             fastk.cpp:128-149) and writes N[u] = t; under the counting rule
+//             also cnt[u] = #{w : E[w] >= t}.
+//   --- grid.sync (a round without a drop ends here, fastk.cpp:109-110) ---
+//   NOTIFY    every dropper u (N[u] < E[u]) re-streams its row against the
+//             SETTLED values N (fastk.cpp:156-163), activates neighbours for
+//             round r+1, and applies E[u] = N[u] (fastk.cpp:153).
+//             Reference rule: activate w iff should_notify(t, cap, N[w]).
+//             Counting rule: if should_notify, atomicSub(cnt[w]); the one
+//             decrement that takes cnt[w] below N[w] activates w.  cnt[v]
+//             stays exactly #{neighbours at or above v's level}, so a vertex
+//             is evaluated iff it will drop: same Jacobi trajectory as the
+//             reference (shadow_run, tests/test_fastk.cpp:41-92), no wasted
+//             evaluations.
+//   --- grid.sync ---
+// No host synchronisation happens between rounds.
 #include <cooperative_groups.h>
 #include <cstdint>
 
@@ -37,8 +44,11 @@ namespace kcb {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-// Chunk sizes (ids) grabbed per atomic, per class.
-constexpr uint32_t CH_BIG = 1, CH_WARP = 8, CH_SUB = 32, CH_THREAD = 256, CH_NOTIFY = 32;
+constexpr uint32_t NWARPS = SOLVE_THREADS / 32;
+// Active vertices grabbed per atomic, per class.
+constexpr uint32_t G_BIG = 2, G_WARP = 8, G_SUB = 32, G_THREAD = 32;
+constexpr uint32_t COMPACT_IDS = SOLVE_THREADS * 16;  // ids per CTA compaction block
+constexpr uint32_t CACHE_MIN_ACTIVE = 4096;  // smaller rounds skip the shared-memory cache
 
 template <typename OffT, typename EstT>
 struct P {
@@ -46,10 +56,11 @@ struct P {
   const uint32_t* adj;
   uint32_t n_nz;
   uint32_t cb[NCLS + 1];
-  EstT* est[2];
-  EstT* old;
+  EstT* E;  // snapshot
+  EstT* N;  // settled
+  uint32_t* cnt;
   uint8_t* flag[2];
-  uint8_t* dropped;
+  uint32_t* queue;
   Ctl* ctl;
   uint32_t* anydrop;
   RoundStat* stats;
@@ -58,18 +69,25 @@ struct P {
   uint32_t r_begin, r_end;
   int rule;
   uint32_t cache_n;
+  uint32_t clamp_drop;  // max degree > H: the reference's round 0 lowers deg -> <= H
 };
 
-// What one round reads and writes (resolved once per round).
+// Per-round view: what this round reads and writes.
 template <typename EstT>
 struct RoundView {
-  const EstT* snap;  // estimates read this round
-  EstT* next;        // snapshot rule: new values of evaluated vertices
-  uint8_t* fcur;     // frontier flags read + cleared this round
-  uint8_t* fnxt;     // activations for the next round
-  uint32_t* grab;    // chunk cursors of this round
-  bool snapshot;     // snapshot rule (else reference rule)
-  bool ext;          // extended_notify
+  const EstT* snap;  // gathered estimates of the current phase (E, then N)
+  uint8_t* fnxt;     // activations for round r+1
+  const uint32_t* qcnt;  // active vertices per class (round r's compacted queue)
+  uint32_t* grab;    // work cursors of the current phase
+  bool count;        // counting rule
+  bool ext;          // extended_notify (reference rule)
+  bool skip_a;       // counting rule, r > 0: every active vertex drops
+  uint32_t cache_n;  // ids cached in shared memory this round (0: none)
+};
+
+struct Acc {  // per-thread counters, flushed per round
+  unsigned long long evals, escan, drops, fires, nscan;
+  bool any_drop;
 };
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
@@ -81,27 +99,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// Estimate of v in this round's snapshot: shared-memory cache for the
-// highest-degree ids, global (L1/L2) otherwise.
-// One generic load per gather (the pointer selects shared or global memory),
-// which keeps the many inlined gather sites small for the instruction cache.
+// Estimate of v: shared-memory cache for the highest-degree ids, global
+// (L1/L2) otherwise.  One generic load per gather keeps the inlined gather
+// sites small for the instruction cache.
 template <typename EstT>
 __device__ __forceinline__ uint32_t est_at(const EstT* __restrict__ s_cache, uint32_t cache_n,
                                            const EstT* snap, uint32_t v) {
-#ifdef KC_NO_SMEM_CACHE
-  (void)s_cache; (void)cache_n;
-  return (uint32_t)snap[v];
-#else
   const EstT* base = v < cache_n ? s_cache : snap;
   return (uint32_t)base[v];
-#endif
-}
-
-// Activation predicate for neighbour estimate x after a drop cap -> t
-// (t < cap): should_notify(t, cap, x) (fastk.hpp:25-27) or, with
-// extended_notify off, the plain guard x > t (fastk.cpp:22-24).
-__device__ __forceinline__ bool fires(bool ext, uint32_t t, uint32_t cap, uint32_t x) {
-  return ext ? (t < x && x <= cap) : (x > t);
 }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
@@ -179,8 +184,6 @@ __device__ __forceinline__ uint32_t u4_get(const uint4& q, int e) {
 // ------------------------------------------------------------------------
 // Block-wide helpers (blockDim == SOLVE_THREADS)
 // ------------------------------------------------------------------------
-constexpr uint32_t NWARPS = SOLVE_THREADS / 32;
-
 __device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* s_red) {
   v = __reduce_add_sync(FULL, v);
   if (lane_id() == 0) s_red[warp_id()] = v;
@@ -221,17 +224,21 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_red)
   return r;
 }
 
-struct Acc {  // per-thread counters, flushed per round
-  unsigned long long evals, escan, drops, fires;
-  bool any_drop;
-};
+// Tally one gathered value into the window [top - NB, top): bin i counts
+// x == top-1-i, `above` counts x >= top (the capped top bin of
+// compute_index_over, kernel.hpp:31-35, kept in registers).
+template <int NB>
+__device__ __forceinline__ void tally(uint32_t x, uint32_t top, uint32_t& above, uint32_t* bins) {
+  if (x >= top) ++above;
+  else if ((int)x >= (int)top - NB) atomicAdd(&bins[top - 1 - x], 1u);
+}
 
-// Windowed histogram step of compute_index_over (kernel.hpp:31-41).  The
-// window holds levels [top - NB, top): bin i counts values x == top-1-i;
-// C counts values >= top.  Returns the smallest bin i whose level
-// x = top-1-i >= 1 satisfies C + sum(bins[0..i]) >= x, or 0xffffffff.
-// Warp version: lane l owns bins [8l, 8l+8).
-__device__ __forceinline__ uint32_t warp_resolve(const uint32_t* bins, uint32_t C, uint32_t top) {
+// Suffix scan of one window (kernel.hpp:36-41): the smallest bin i whose
+// level x = top-1-i >= 1 has count(>= x) = C + sum(bins[0..i]) >= x.  Warp
+// version, lane l owns bins [8l, 8l+8).  Returns the level and, in `cnt`,
+// count(>= level).
+__device__ __forceinline__ bool warp_resolve(const uint32_t* bins, uint32_t C, uint32_t top,
+                                             uint32_t& level, uint32_t& cnt) {
   static_assert(WARP_BINS == 256, "8 bins per lane");
   const uint32_t lane = lane_id();
   const uint4 b0 = reinterpret_cast<const uint4*>(bins)[2 * lane];
@@ -241,15 +248,22 @@ __device__ __forceinline__ uint32_t warp_resolve(const uint32_t* bins, uint32_t 
 #pragma unroll
   for (int j = 0; j < 8; ++j) s += b[j];
   uint32_t run = C + warp_incl_scan(s) - s;
-  uint32_t found = 0xffffffffu;
+  uint32_t found = 0xffffffffu, frun = 0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     run += b[j];
     const int i = (int)lane * 8 + j;
     const int x = (int)top - 1 - i;
-    if (found == 0xffffffffu && x >= 1 && run >= (uint32_t)x) found = (uint32_t)i;
+    if (found == 0xffffffffu && x >= 1 && run >= (uint32_t)x) {
+      found = (uint32_t)i;
+      frun = run;
+    }
   }
-  return __reduce_min_sync(FULL, found);
+  const uint32_t g = __reduce_min_sync(FULL, found);
+  if (g == 0xffffffffu) return false;
+  cnt = __shfl_sync(FULL, frun, g >> 3);
+  level = top - 1 - g;
+  return true;
 }
 
 __device__ __forceinline__ void warp_zero_bins(uint32_t* bins) {
@@ -257,13 +271,6 @@ __device__ __forceinline__ void warp_zero_bins(uint32_t* bins) {
   reinterpret_cast<uint4*>(bins)[2 * lane] = make_uint4(0, 0, 0, 0);
   reinterpret_cast<uint4*>(bins)[2 * lane + 1] = make_uint4(0, 0, 0, 0);
   __syncwarp();
-}
-
-// Tally one gathered value into the window [top - NB, top).
-template <int NB>
-__device__ __forceinline__ void tally(uint32_t x, uint32_t top, uint32_t& above, uint32_t* bins) {
-  if (x >= top) ++above;
-  else if ((int)x >= (int)top - NB) atomicAdd(&bins[top - 1 - x], 1u);
 }
 
 // ------------------------------------------------------------------------
@@ -303,125 +310,193 @@ __device__ __forceinline__ void stream_row(const P<OffT, EstT>& p, const EstT* s
   }
 }
 
-// Record one evaluation result.  Snapshot rule: write the new value of every
-// evaluated vertex (keeps the double buffer current) and self-activate on a
-// drop.  Reference rule: droppers record new/old values and a dropped mark
-// for the apply and notify phases.
+// One evaluation result (the evaluate phase): lower N[u], keep cnt[u] exact.
 template <typename OffT, typename EstT>
 __device__ __forceinline__ void finish_eval(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
-                                            uint32_t u, uint32_t t, uint32_t cap, Acc& acc) {
-  if (rv.snapshot) {
-    rv.next[u] = (EstT)t;
-    if (t < cap) rv.fnxt[u] = 1;
-  } else if (t < cap) {
-    p.est[1][u] = (EstT)t;
-    p.old[u] = (EstT)cap;
-    p.dropped[u] = 1;
-  }
+                                            uint32_t u, uint32_t t, uint32_t cap, uint32_t c,
+                                            uint64_t deg, Acc& acc) {
+  acc.evals += 1;
+  acc.escan += deg;
+  if (rv.count) p.cnt[u] = c;
   if (t < cap) {
+    p.N[u] = (EstT)t;
     acc.drops += 1;
     acc.any_drop = true;
   }
 }
 
-// ------------------------------------------------------------------------
-// Frontier scan: a warp grabs CH ids of class `cls` at a time, reads their
-// flags four per lane (one 32-bit load), clears the set ones, and hands
-// batches of up to 32 active ids (compacted in the warp's shared list) to
-// `proc(list, n)`.
-// ------------------------------------------------------------------------
-template <uint32_t CH, bool ACCUM, typename F>
-__device__ __forceinline__ void scan_class(uint8_t* flags, uint32_t* grab, uint32_t b0,
-                                           uint32_t b1, uint32_t* list, F&& proc) {
-  const uint32_t lane = lane_id();
-  uint32_t cnt = 0;  // warp-uniform
-  for (;;) {
-    uint32_t start = 0;
-    if (lane == 0) start = atomicAdd(grab, CH);
-    start = __shfl_sync(FULL, start, 0);
-    const uint32_t lo = b0 + start;
-    if (start >= b1 - b0) break;
-    const uint32_t hi = lo + CH < b1 ? lo + CH : b1;
-    for (uint32_t s = lo & ~3u; s < hi; s += 128) {
-      const uint32_t a = s + 4 * lane;
-      uint32_t w = a < hi ? *reinterpret_cast<const uint32_t*>(flags + a) : 0u;
+// What a dropper u (cap -> t) does to K neighbours ids[k] with settled
+// levels x[k] (valid where bit k of ok) in the notify phase.  All counter
+// atomics are issued before any result is consumed (a byte store to the
+// flags could alias cnt, so interleaving would serialise them).
+template <int K, typename OffT, typename EstT>
+__device__ __forceinline__ void notify_batch(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
+                                             uint32_t ok, const uint32_t (&ids)[K],
+                                             const uint32_t (&x)[K], uint32_t t, uint32_t cap,
+                                             Acc& acc) {
+  uint32_t fire = 0;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const uint32_t id = a + b;
-        const bool act = (w >> (8 * b) & 0xffu) && id >= lo && id < hi;
-        if (act) flags[id] = 0;
-        const uint32_t m = __ballot_sync(FULL, act);
-        if (act) list[cnt + __popc(m & lanemask_lt())] = id;
-        cnt += __popc(m);
-        if (cnt >= 32) {
-          __syncwarp();
-          proc(list, 32u);
-          __syncwarp();
-          if (lane < cnt - 32) list[lane] = list[32 + lane];
-          __syncwarp();
-          cnt -= 32;
-        }
-      }
-    }
-    if (!ACCUM && cnt) {  // warp-per-vertex classes: no batching across chunks
-      __syncwarp();
-      proc(list, cnt);
-      __syncwarp();
-      cnt = 0;
-    }
+  for (int k = 0; k < K; ++k) {
+    const bool f = (ok >> k & 1) && (rv.count || rv.ext ? (t < x[k] && x[k] <= cap) : (x[k] > t));
+    fire |= (uint32_t)f << k;
   }
-  if (cnt) {
-    __syncwarp();
-    proc(list, cnt);
-    __syncwarp();
+  acc.fires += __popc(fire);
+  if (rv.count) {  // should_notify on the settled value -> decrement cnt[w]
+    uint32_t old[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) old[k] = (fire >> k & 1) ? atomicSub(&p.cnt[ids[k]], 1u) : 0u;
+#pragma unroll
+    for (int k = 0; k < K; ++k)  // the decrement that took cnt[w] below N[w]
+      if ((fire >> k & 1) && old[k] == x[k]) rv.fnxt[ids[k]] = 1;
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (fire >> k & 1) rv.fnxt[ids[k]] = 1;
   }
 }
 
 // ------------------------------------------------------------------------
-// HUGE class: CTA per vertex (deg > DEG_BIG_MAX).  Pass A only counts
-// values >= cap in registers ("no change" — the common case after the first
-// rounds — costs one read of the row and one block reduction).  A drop runs
-// windowed histogram passes: values >= top in registers, the window
-// [top - HIST_BINS, top) binned in shared memory; then, under the snapshot
-// rule, one more pass activates neighbours.  Re-reads hit L2.
+// Frontier compaction (round start, all CTAs): round r's flags become a
+// dense per-class queue.  CTAs take interleaved blocks of COMPACT_IDS ids,
+// each thread reads 16 flags with one 128-bit load and clears them; one
+// atomicAdd per CTA block reserves the block's slots in the class segment.
 // ------------------------------------------------------------------------
 template <typename OffT, typename EstT>
-__device__ __noinline__ uint32_t huge_window(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
-                                             const EstT* s_cache, uint32_t* s_hist,
-                                             uint32_t* s_red, uint64_t ob, uint64_t oe,
-                                             uint32_t cap) {
+__device__ void compact_frontier(const P<OffT, EstT>& p, uint8_t* flags, uint32_t* qcnt,
+                                 uint32_t* s_red, uint32_t* s_item) {
+  const uint32_t tid = threadIdx.x;
+  for (int c = 0; c < NCLS; ++c) {
+    const uint32_t b0 = p.cb[c], b1 = p.cb[c + 1];
+    const uint32_t a0 = b0 & ~15u;
+    const uint32_t nblk = (b1 - a0 + COMPACT_IDS - 1) / COMPACT_IDS;
+    for (uint32_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+      const uint32_t a = a0 + blk * COMPACT_IDS + 16 * tid;
+      uint4 w = make_uint4(0, 0, 0, 0);
+      if (a < b1) w = *reinterpret_cast<const uint4*>(flags + a);
+      uint32_t m = 0;  // bit j: id a+j active and inside the class
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t word = j < 4 ? w.x : j < 8 ? w.y : j < 12 ? w.z : w.w;
+        const uint32_t id = a + j;
+        if ((word >> (8 * (j & 3)) & 0xffu) && id >= b0 && id < b1) m |= 1u << j;
+      }
+      const uint32_t mine = __popc(m);
+      const uint32_t off = block_excl_scan(mine, s_red);
+      if (tid == SOLVE_THREADS - 1) {
+        const uint32_t tot = off + mine;
+        *s_item = tot ? atomicAdd(&qcnt[c], tot) : 0u;
+      }
+      __syncthreads();
+      uint32_t pos = b0 + *s_item + off;
+      __syncthreads();
+      if (m) {
+        // clear exactly this class's bytes of the 16 (a neighbouring class
+        // may share the 16-byte granule)
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (m >> j & 1) {
+            p.queue[pos++] = a + j;
+            flags[a + j] = 0;
+          }
+      }
+    }
+  }
+}
+
+// Warp-level dense-queue grab: up to G (<= 32) items per atomic; `proc` gets
+// the warp's slice (lane i may read q[i] for i < n).
+template <uint32_t G, typename F>
+__device__ __forceinline__ void for_queue(const uint32_t* q, uint32_t cnt, uint32_t* cursor,
+                                          F&& proc) {
+  static_assert(G <= 32, "one item per lane at most");
+  if (cnt == 0) return;
+  for (;;) {
+    uint32_t base = 0;
+    if (lane_id() == 0)  // plain read first: no atomic once the queue is drained
+      base = *reinterpret_cast<volatile uint32_t*>(cursor) >= cnt ? cnt : atomicAdd(cursor, G);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= cnt) break;
+    proc(q + base, cnt - base < G ? cnt - base : G);
+  }
+}
+
+// CTA-level grab of the next queued HUGE vertex (0xffffffff when none).
+template <typename OffT, typename EstT>
+__device__ __forceinline__ uint32_t grab_huge(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
+                                              uint32_t* s_item) {
+  if (threadIdx.x == 0) {
+    const uint32_t cnt = rv.qcnt[C_HUGE];
+    const uint32_t k = (cnt == 0 || *reinterpret_cast<volatile uint32_t*>(&rv.grab[C_HUGE]) >= cnt)
+                           ? cnt
+                           : atomicAdd(&rv.grab[C_HUGE], 1u);
+    *s_item = k < cnt ? p.queue[p.cb[C_HUGE] + k] : 0xffffffffu;
+  }
+  __syncthreads();
+  const uint32_t u = *s_item;
+  __syncthreads();
+  return u;
+}
+
+// ------------------------------------------------------------------------
+// HUGE class (deg > DEG_BIG_MAX): CTA per vertex.  Pass A counts values >=
+// cap in registers ("no change" costs one read + one block reduction); a drop
+// runs windowed histogram passes (values >= top in registers, the window
+// [top - HIST_BINS, top) binned in shared memory).  Re-reads hit L2.
+// ------------------------------------------------------------------------
+template <typename OffT, typename EstT>
+__device__ __noinline__ void huge_window(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
+                                         const EstT* s_cache, uint32_t* s_hist, uint32_t* s_red,
+                                         uint64_t ob, uint64_t oe, uint32_t cap, uint32_t* out) {
   const uint32_t tid = threadIdx.x;
   uint32_t top = cap;
   for (;;) {
     for (int i = tid; i < HIST_BINS; i += SOLVE_THREADS) s_hist[i] = 0;
     __syncthreads();
     uint32_t above = 0;
-    stream_row<SOLVE_THREADS>(p, rv.snap, tid, ob, oe, s_cache, p.cache_n,
+    stream_row<SOLVE_THREADS>(p, rv.snap, tid, ob, oe, s_cache, rv.cache_n,
                               [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
                                 for (int k = 0; k < 8; ++k)
                                   if (ok >> k & 1) tally<HIST_BINS>(x[k], top, above, s_hist);
                               });
     const uint32_t C = block_sum(above, s_red);
-    uint32_t h[HIST_BINS / SOLVE_THREADS];
+    constexpr int PER = HIST_BINS / SOLVE_THREADS;
+    uint32_t h[PER];
     uint32_t sm = 0;
 #pragma unroll
-    for (int j = 0; j < HIST_BINS / SOLVE_THREADS; ++j) {
-      h[j] = s_hist[tid * (HIST_BINS / SOLVE_THREADS) + j];
+    for (int j = 0; j < PER; ++j) {
+      h[j] = s_hist[tid * PER + j];
       sm += h[j];
     }
     uint32_t run = C + block_excl_scan(sm, s_red);
-    uint32_t found = 0xffffffffu;
+    uint32_t found = 0xffffffffu, frun = 0;
 #pragma unroll
-    for (int j = 0; j < HIST_BINS / SOLVE_THREADS; ++j) {
+    for (int j = 0; j < PER; ++j) {
       run += h[j];
-      const int i = tid * (HIST_BINS / SOLVE_THREADS) + j;
+      const int i = tid * PER + j;
       const int x = (int)top - 1 - i;
-      if (found == 0xffffffffu && x >= 1 && run >= (uint32_t)x) found = (uint32_t)i;
+      if (found == 0xffffffffu && x >= 1 && run >= (uint32_t)x) {
+        found = (uint32_t)i;
+        frun = run;
+      }
     }
-    found = block_min(found, s_red);
-    if (found != 0xffffffffu) return top - 1 - found;
-    if ((int)top - HIST_BINS <= 0) return 0;
+    const uint32_t g = block_min(found, s_red);
+    if (g != 0xffffffffu) {
+      if (found == g) {
+        out[0] = top - 1 - g;
+        out[1] = frun;
+      }
+      __syncthreads();
+      return;
+    }
+    if ((int)top - HIST_BINS <= 0) {
+      if (tid == 0) {
+        out[0] = 0;
+        out[1] = (uint32_t)(oe - ob);
+      }
+      __syncthreads();
+      return;
+    }
     top -= HIST_BINS;
   }
 }
@@ -430,51 +505,31 @@ template <typename OffT, typename EstT>
 __device__ void eval_huge(const P<OffT, EstT>& p, const RoundView<EstT>& rv, const EstT* s_cache,
                           uint32_t* s_hist, uint32_t* s_red, uint32_t* s_item, Acc& acc) {
   const uint32_t tid = threadIdx.x;
-  const uint32_t b0 = p.cb[C_HUGE], b1 = p.cb[C_HUGE + 1];
+  __shared__ uint32_t s_out[2];
   for (;;) {
-    if (tid == 0) {
-      uint32_t u = 0xffffffffu;
-      for (;;) {  // next active HUGE vertex
-        const uint32_t k = atomicAdd(&rv.grab[C_HUGE], 1u);
-        if (k >= b1 - b0) break;
-        if (rv.fcur[b0 + k]) {
-          rv.fcur[b0 + k] = 0;
-          u = b0 + k;
-          break;
-        }
-      }
-      *s_item = u;
-    }
-    __syncthreads();
-    const uint32_t u = *s_item;
-    __syncthreads();
+    const uint32_t u = grab_huge(p, rv, s_item);
     if (u == 0xffffffffu) break;
     const uint64_t ob = p.off[u], oe = p.off[u + 1];
-    const uint32_t cap = est_at(s_cache, p.cache_n, rv.snap, u);
-    uint32_t c = 0;
-    stream_row<SOLVE_THREADS>(p, rv.snap, tid, ob, oe, s_cache, p.cache_n,
-                              [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
+    const uint32_t cap = est_at(s_cache, rv.cache_n, rv.snap, u);
+    bool keep = false;
+    uint32_t cA = 0;
+    if (!rv.skip_a) {
+      uint32_t c = 0;
+      stream_row<SOLVE_THREADS>(p, rv.snap, tid, ob, oe, s_cache, rv.cache_n,
+                                [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
-                                for (int k = 0; k < 8; ++k) c += (ok >> k & 1) && x[k] >= cap;
-                              });
-    uint32_t t = cap;
-    if (block_sum(c, s_red) < cap) t = huge_window(p, rv, s_cache, s_hist, s_red, ob, oe, cap);
-    if (tid == 0) {
-      acc.evals += 1;
-      acc.escan += oe - ob;
-      finish_eval(p, rv, u, t, cap, acc);
-    }
-    if (t < cap && rv.snapshot) {  // re-stream the row (L2-resident) and activate
-      stream_row<SOLVE_THREADS>(p, rv.snap, tid, ob, oe, s_cache, p.cache_n,
-                                [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
-#pragma unroll
-                                  for (int k = 0; k < 8; ++k)
-                                    if ((ok >> k & 1) && fires(rv.ext, t, cap, x[k])) {
-                                      rv.fnxt[ids[k]] = 1;
-                                      acc.fires += 1;
-                                    }
+                                  for (int k = 0; k < 8; ++k) c += (ok >> k & 1) && x[k] >= cap;
                                 });
+      cA = block_sum(c, s_red);
+      keep = cA >= cap;
     }
+    uint32_t t = cap, cn = cA;
+    if (!keep) {
+      huge_window(p, rv, s_cache, s_hist, s_red, ob, oe, cap, s_out);
+      t = s_out[0];
+      cn = s_out[1];
+    }
+    if (tid == 0) finish_eval(p, rv, u, t, cap, cn, oe - ob, acc);
     __syncthreads();
   }
 }
@@ -490,15 +545,16 @@ struct Meta {
 };
 
 template <typename OffT, typename EstT>
-__device__ __forceinline__ Meta load_meta(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
-                                          const EstT* s_cache, const uint32_t* list, uint32_t n) {
+__device__ __forceinline__ Meta load_meta(const P<OffT, EstT>& p, const EstT* capsrc,
+                                          const EstT* s_cache, uint32_t cache_n,
+                                          const uint32_t* q, uint32_t n) {
   Meta m{0, 0, 0, 0};
   const uint32_t lane = lane_id();
   if (lane < n) {
-    m.u = list[lane];
+    m.u = q[lane];
     m.ob = p.off[m.u];
     m.oe = p.off[m.u + 1];
-    m.cap = est_at(s_cache, p.cache_n, rv.snap, m.u);
+    m.cap = est_at(s_cache, cache_n, capsrc, m.u);
   }
   return m;
 }
@@ -512,18 +568,17 @@ __device__ __forceinline__ Meta shfl_meta(const Meta& m, int src) {
   return it;
 }
 
-// Windowed histogram passes of one warp over a row (after pass A found a
-// drop): returns the capped h-index.
+// Windowed histogram passes of one warp over a row: capped h-index + count.
 template <typename OffT, typename EstT>
-__device__ __noinline__ uint32_t warp_window(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
-                                             const EstT* s_cache, uint32_t* bins, uint64_t ob,
-                                             uint64_t oe, uint32_t cap) {
+__device__ __noinline__ uint2 warp_window(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
+                                          const EstT* s_cache, uint32_t* bins, uint64_t ob,
+                                          uint64_t oe, uint32_t cap) {
   const uint32_t lane = lane_id();
   uint32_t top = cap;
   for (;;) {
     warp_zero_bins(bins);
     uint32_t above = 0;
-    stream_row<32>(p, rv.snap, lane, ob, oe, s_cache, p.cache_n,
+    stream_row<32>(p, rv.snap, lane, ob, oe, s_cache, rv.cache_n,
                    [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
                      for (int k = 0; k < 8; ++k)
@@ -531,57 +586,49 @@ __device__ __noinline__ uint32_t warp_window(const P<OffT, EstT>& p, const Round
                    });
     __syncwarp();
     const uint32_t C = __reduce_add_sync(FULL, above);
-    const uint32_t found = warp_resolve(bins, C, top);
+    uint32_t level = 0, c = 0;
+    const bool hit = warp_resolve(bins, C, top, level, c);
     __syncwarp();
-    if (found != 0xffffffffu) return top - 1 - found;
-    if ((int)top - WARP_BINS <= 0) return 0;
+    if (hit) return make_uint2(level, c);
+    if ((int)top - WARP_BINS <= 0) return make_uint2(0u, (uint32_t)(oe - ob));
     top -= WARP_BINS;
   }
 }
 
-// WARP and BIG classes: warp per vertex (DEG_SUB_MAX < deg <= DEG_BIG_MAX),
+// WARP and BIG classes (DEG_SUB_MAX < deg <= DEG_BIG_MAX): warp per vertex,
 // 256 entries per warp step (two 128-bit id loads + 8 gathers per lane).
-template <uint32_t CH, typename OffT, typename EstT>
+template <uint32_t G, typename OffT, typename EstT>
 __device__ void eval_wstream(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
-                             const EstT* s_cache, int cls, uint32_t* bins, uint32_t* list,
-                             Acc& acc) {
+                             const EstT* s_cache, int cls, uint32_t* bins, Acc& acc) {
   const uint32_t lane = lane_id();
-  scan_class<CH, false>(rv.fcur, &rv.grab[cls], p.cb[cls], p.cb[cls + 1], list,
-                        [&](const uint32_t* lst, uint32_t n) {
-    const Meta mine = load_meta(p, rv, s_cache, lst, n);
+  for_queue<G>(p.queue + p.cb[cls], rv.qcnt[cls], &rv.grab[cls],
+               [&](const uint32_t* lst, uint32_t n) {
+    const Meta mine = load_meta(p, rv.snap, s_cache, rv.cache_n, lst, n);
     for (uint32_t i = 0; i < n; ++i) {
       const Meta it = shfl_meta(mine, i);
       const uint32_t cap = it.cap;
-      uint32_t c = 0;
-      stream_row<32>(p, rv.snap, lane, it.ob, it.oe, s_cache, p.cache_n,
-                     [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
+      bool keep = false;
+      uint32_t cA = 0;
+      if (!rv.skip_a) {
+        uint32_t c = 0;
+        stream_row<32>(p, rv.snap, lane, it.ob, it.oe, s_cache, rv.cache_n,
+                       [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
-                       for (int k = 0; k < 8; ++k) c += (ok >> k & 1) && x[k] >= cap;
-                     });
-      uint32_t t = cap;
-      if (__reduce_add_sync(FULL, c) < cap) t = warp_window(p, rv, s_cache, bins, it.ob, it.oe, cap);
-      if (lane == 0) {
-        acc.evals += 1;
-        acc.escan += it.oe - it.ob;
-        finish_eval(p, rv, it.u, t, cap, acc);
-      }
-      if (t < cap && rv.snapshot) {
-        stream_row<32>(p, rv.snap, lane, it.ob, it.oe, s_cache, p.cache_n,
-                       [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
-#pragma unroll
-                         for (int k = 0; k < 8; ++k)
-                           if ((ok >> k & 1) && fires(rv.ext, t, cap, x[k])) {
-                             rv.fnxt[ids[k]] = 1;
-                             acc.fires += 1;
-                           }
+                         for (int k = 0; k < 8; ++k) c += (ok >> k & 1) && x[k] >= cap;
                        });
+        cA = __reduce_add_sync(FULL, c);
+        keep = cA >= cap;
       }
+      uint2 tc = make_uint2(cap, cA);
+      if (!keep) tc = warp_window(p, rv, s_cache, bins, it.ob, it.oe, cap);
+      if (lane == 0) finish_eval(p, rv, it.u, tc.x, cap, tc.y, it.oe - it.ob, acc);
     }
   });
 }
 
 // ------------------------------------------------------------------------
-// SUB class: 8-lane tile per vertex (4 vertices per warp), 8 values per lane.
+// SUB class (DEG_THREAD_MAX < deg <= DEG_SUB_MAX): 8-lane tile per vertex
+// (4 vertices per warp), 8 values per lane in registers, bisection.
 // ------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t tile8_sum(uint32_t v) {
   v += __shfl_xor_sync(FULL, v, 4, 8);
@@ -592,32 +639,33 @@ __device__ __forceinline__ uint32_t tile8_sum(uint32_t v) {
 
 template <typename OffT, typename EstT>
 __device__ void eval_sub(const P<OffT, EstT>& p, const RoundView<EstT>& rv, const EstT* s_cache,
-                         uint32_t* list, Acc& acc) {
+                         Acc& acc) {
   constexpr int R = DEG_SUB_MAX / 8;
-  const uint32_t lane = lane_id(), g = lane >> 3, k = lane & 7;
-  scan_class<CH_SUB, true>(rv.fcur, &rv.grab[C_SUB], p.cb[C_SUB], p.cb[C_SUB + 1], list,
-                     [&](const uint32_t* lst, uint32_t n) {
-    const Meta mine = load_meta(p, rv, s_cache, lst, n);
+  const uint32_t g = lane_id() >> 3, k = lane_id() & 7;
+  for_queue<G_SUB>(p.queue + p.cb[C_SUB], rv.qcnt[C_SUB], &rv.grab[C_SUB],
+                   [&](const uint32_t* lst, uint32_t n) {
+    const Meta mine = load_meta(p, rv.snap, s_cache, rv.cache_n, lst, n);
     for (uint32_t i0 = 0; i0 < n; i0 += 4) {
       // every lane runs the shuffles; tiles beyond n idle
       const Meta it = shfl_meta(mine, (int)(i0 + g) & 31);
       const bool has = i0 + g < n;
-      const uint32_t u = it.u;
       const uint32_t deg = has ? (uint32_t)(it.oe - it.ob) : 0u;
       const uint32_t cap = has ? it.cap : 0u;
-      uint32_t ids[R];
       Vals<EstT, R> vals;
       vals.clear();
+      {
+        uint32_t ids[R];
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        const uint32_t q = k + 8 * j;
-        ids[j] = q < deg ? p.adj[it.ob + q] : 0xffffffffu;
+        for (int j = 0; j < R; ++j) {
+          const uint32_t q = k + 8 * j;
+          ids[j] = q < deg ? p.adj[it.ob + q] : 0xffffffffu;
+        }
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          if (ids[j] != 0xffffffffu) vals.set(j, est_at(s_cache, rv.cache_n, rv.snap, ids[j]));
       }
-#pragma unroll
-      for (int j = 0; j < R; ++j)
-        if (ids[j] != 0xffffffffu) vals.set(j, est_at(s_cache, p.cache_n, rv.snap, ids[j]));
       // capped h-index by bisection, all four tiles in lockstep
-      const bool keep = tile8_sum(vals.count_ge(cap)) >= cap;
+      const uint32_t cA = tile8_sum(vals.count_ge(cap));
       uint32_t lo = 0, hi = cap;
 #pragma unroll 1
       for (int s = 0; s < 7; ++s) {  // cap <= 64
@@ -627,46 +675,35 @@ __device__ void eval_sub(const P<OffT, EstT>& p, const RoundView<EstT>& rv, cons
           if (okm) lo = mid; else hi = mid;
         }
       }
-      const uint32_t t = keep ? cap : lo;
-      if (has && k == 0) {
-        acc.evals += 1;
-        acc.escan += deg;
-        finish_eval(p, rv, u, t, cap, acc);
-      }
-      if (has && t < cap && rv.snapshot) {
-#pragma unroll
-        for (int j = 0; j < R; ++j)
-          if (ids[j] != 0xffffffffu && fires(rv.ext, t, cap, vals.get(j))) {
-            rv.fnxt[ids[j]] = 1;
-            acc.fires += 1;
-          }
-      }
+      const uint32_t t = cA >= cap ? cap : lo;
+      const uint32_t c = tile8_sum(vals.count_ge(t));
+      if (has && k == 0) finish_eval(p, rv, it.u, t, cap, c, deg, acc);
     }
   });
 }
 
 // ------------------------------------------------------------------------
-// THREAD class: one thread per vertex (deg <= 8), h-index = max_i min(x_i,
-// #{j : x_j >= x_i}) — the classic h-index identity, capped at est[u].
+// THREAD class (deg <= DEG_THREAD_MAX): thread per vertex.  h-index =
+// max_i min(x_i, #{j : x_j >= x_i}) — the classic identity — capped at cap.
 // ------------------------------------------------------------------------
 template <typename OffT, typename EstT>
 __device__ void eval_thread(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
-                            const EstT* s_cache, uint32_t* list, Acc& acc) {
+                            const EstT* s_cache, Acc& acc) {
   constexpr int R = DEG_THREAD_MAX;
   const uint32_t lane = lane_id();
-  scan_class<CH_THREAD, true>(rv.fcur, &rv.grab[C_THREAD], p.cb[C_THREAD], p.cb[C_THREAD + 1], list,
-                        [&](const uint32_t* lst, uint32_t n) {
+  for_queue<G_THREAD>(p.queue + p.cb[C_THREAD], rv.qcnt[C_THREAD], &rv.grab[C_THREAD],
+                      [&](const uint32_t* lst, uint32_t n) {
     if (lane >= n) return;
     const uint32_t u = lst[lane];
     const uint64_t ob = p.off[u];
     const uint32_t deg = (uint32_t)(p.off[u + 1] - ob);
-    const uint32_t cap = est_at(s_cache, p.cache_n, rv.snap, u);
-    uint32_t ids[R], x[R];
+    const uint32_t cap = est_at(s_cache, rv.cache_n, rv.snap, u);
+    uint32_t x[R];
 #pragma unroll
-    for (int j = 0; j < R; ++j) ids[j] = (uint32_t)j < deg ? p.adj[ob + j] : 0xffffffffu;
-#pragma unroll
-    for (int j = 0; j < R; ++j)
-      x[j] = ids[j] != 0xffffffffu ? est_at(s_cache, p.cache_n, rv.snap, ids[j]) : 0u;
+    for (int j = 0; j < R; ++j) {
+      const uint32_t id = (uint32_t)j < deg ? p.adj[ob + j] : 0xffffffffu;
+      x[j] = id != 0xffffffffu ? est_at(s_cache, rv.cache_n, rv.snap, id) : 0u;
+    }
     uint32_t h = 0;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -677,43 +714,89 @@ __device__ void eval_thread(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
       h = m > h ? m : h;
     }
     const uint32_t t = h < cap ? h : cap;
-    acc.evals += 1;
-    acc.escan += deg;
-    finish_eval(p, rv, u, t, cap, acc);
-    if (t < cap && rv.snapshot) {
+    uint32_t c = 0;
 #pragma unroll
-      for (int j = 0; j < R; ++j)
-        if (ids[j] != 0xffffffffu && fires(rv.ext, t, cap, x[j])) {
-          rv.fnxt[ids[j]] = 1;
-          acc.fires += 1;
-        }
-    }
+    for (int j = 0; j < R; ++j) c += x[j] >= t;
+    finish_eval(p, rv, u, t, cap, t ? c : deg, deg, acc);
   });
 }
 
 // ------------------------------------------------------------------------
-// Reference rule, after the apply barrier: re-stream every dropper's row
-// and activate on SETTLED estimates (fastk.cpp:156-163); warp per dropper.
+// NOTIFY phase: every dropper u of round r (flag set, N[u] < E[u]) streams
+// its row against the settled values N, activates neighbours for round r+1
+// (notify_one) and applies E[u] = N[u].  All of round r's flags are cleared.
+// Gathers go through the shared-memory cache of N.
 // ------------------------------------------------------------------------
 template <typename OffT, typename EstT>
-__device__ void notify_settled(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
-                               uint32_t* list, Acc& acc) {
-  const uint32_t lane = lane_id();
-  scan_class<CH_NOTIFY, false>(p.dropped, &rv.grab[NCLS], 0u, p.n_nz, list,
-                        [&](const uint32_t* lst, uint32_t n) {
-    for (uint32_t i = 0; i < n; ++i) {
-      const uint32_t u = lst[i];
-      const uint32_t t = p.est[0][u], oc = p.old[u];
+__device__ void notify_huge(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
+                            const EstT* s_cache, uint32_t* s_item, Acc& acc) {
+  const uint32_t tid = threadIdx.x;
+  for (;;) {
+    const uint32_t u = grab_huge(p, rv, s_item);
+    if (u == 0xffffffffu) break;
+    const uint32_t t = p.N[u], cap = p.E[u];
+    if (t < cap) {
       const uint64_t ob = p.off[u], oe = p.off[u + 1];
-      stream_row<32>(p, p.est[0], lane, ob, oe, (const EstT*)nullptr, 0u,
+      if (tid == 0) acc.nscan += oe - ob;
+      stream_row<SOLVE_THREADS>(p, p.N, tid, ob, oe, s_cache, rv.cache_n,
+                                [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
+                                  notify_batch<8>(p, rv, ok, ids, x, t, cap, acc);
+                                });
+      if (tid == 0) p.E[u] = (EstT)t;  // apply (fastk.cpp:153)
+    }
+    __syncthreads();
+  }
+}
+
+template <uint32_t G, typename OffT, typename EstT>
+__device__ void notify_wstream(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
+                               const EstT* s_cache, int cls, Acc& acc) {
+  const uint32_t lane = lane_id();
+  for_queue<G>(p.queue + p.cb[cls], rv.qcnt[cls], &rv.grab[cls],
+               [&](const uint32_t* lst, uint32_t n) {
+    Meta mine = load_meta(p, (const EstT*)p.E, (const EstT*)nullptr, 0u, lst, n);  // cap = old E
+    const uint32_t tn = lane < n ? (uint32_t)p.N[mine.u] : 0u;
+    for (uint32_t i = 0; i < n; ++i) {
+      const Meta it = shfl_meta(mine, i);
+      const uint32_t t = __shfl_sync(FULL, tn, i);
+      if (t >= it.cap) continue;  // evaluated but did not drop (warp-uniform)
+      if (lane == 0) acc.nscan += it.oe - it.ob;
+      stream_row<32>(p, (const EstT*)p.N, lane, it.ob, it.oe, s_cache, rv.cache_n,
                      [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
-#pragma unroll
-                       for (int j = 0; j < 8; ++j)
-                         if ((ok >> j & 1) && fires(rv.ext, t, oc, x[j])) {
-                           rv.fnxt[ids[j]] = 1;
-                           acc.fires += 1;
-                         }
+                       notify_batch<8>(p, rv, ok, ids, x, t, it.cap, acc);
                      });
+      if (lane == 0) p.E[it.u] = (EstT)t;
+    }
+  });
+}
+
+// SUB and THREAD droppers: 8-lane tile per dropper, up to 8 neighbours per lane.
+template <uint32_t G, typename OffT, typename EstT>
+__device__ void notify_small(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
+                             const EstT* s_cache, int cls, Acc& acc) {
+  const uint32_t g = lane_id() >> 3, k = lane_id() & 7;
+  for_queue<G>(p.queue + p.cb[cls], rv.qcnt[cls], &rv.grab[cls],
+               [&](const uint32_t* lst, uint32_t n) {
+    for (uint32_t i0 = 0; i0 < n; i0 += 4) {
+      if (i0 + g >= n) continue;
+      const uint32_t u = lst[i0 + g];
+      const uint32_t t = p.N[u], cap = p.E[u];
+      if (t >= cap) continue;
+      const uint64_t ob = p.off[u];
+      const uint32_t deg = (uint32_t)(p.off[u + 1] - ob);
+      if (k == 0) acc.nscan += deg;
+      uint32_t ids[8], x[8], ok = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool v = k + 8u * j < deg;
+        ids[j] = v ? p.adj[ob + k + 8u * j] : 0u;
+        ok |= (uint32_t)v << j;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        x[j] = (ok >> j & 1) ? est_at(s_cache, rv.cache_n, (const EstT*)p.N, ids[j]) : 0u;
+      notify_batch<8>(p, rv, ok, ids, x, t, cap, acc);
+      if (k == 0) p.E[u] = (EstT)t;
     }
   });
 }
@@ -721,9 +804,9 @@ __device__ void notify_settled(const P<OffT, EstT>& p, const RoundView<EstT>& rv
 template <typename OffT, typename EstT>
 __device__ __forceinline__ void flush_acc(const P<OffT, EstT>& p, uint32_t sr, const Acc& acc,
                                           unsigned long long* s_acc) {
-  unsigned long long v[4] = {acc.evals, acc.escan, acc.drops, acc.fires};
+  const unsigned long long v[5] = {acc.evals, acc.escan, acc.drops, acc.fires, acc.nscan};
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < 5; ++q) {
     unsigned long long x = v[q];
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(FULL, x, d);
@@ -732,8 +815,30 @@ __device__ __forceinline__ void flush_acc(const P<OffT, EstT>& p, uint32_t sr, c
   __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 5; ++q)
       if (s_acc[q]) atomicAdd(&p.stats[sr].evals + q, s_acc[q]);
+  }
+}
+
+template <typename EstT>
+__device__ __forceinline__ void fill_cache(EstT* s_cache, const EstT* src, uint32_t cache_n) {
+  // cache_n * sizeof(EstT) is a multiple of 16 bytes; 8 loads in flight per
+  // thread so the fill costs ~2 memory round trips, not nvec / SOLVE_THREADS
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(s_cache);
+  const uint32_t nvec = (uint32_t)((size_t)cache_n * sizeof(EstT) / 16);
+  for (uint32_t i0 = threadIdx.x; i0 < nvec; i0 += 8 * SOLVE_THREADS) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t i = i0 + k * SOLVE_THREADS;
+      if (i < nvec) v[k] = s[i];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t i = i0 + k * SOLVE_THREADS;
+      if (i < nvec) d[i] = v[k];
+    }
   }
 }
 
@@ -744,102 +849,105 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) rounds_kernel(P<OffT, EstT> 
   EstT* s_cache = reinterpret_cast<EstT*>(smem);
   const size_t cache_bytes = ((size_t)p.cache_n * sizeof(EstT) + 15) & ~(size_t)15;
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(smem + cache_bytes);
-  // per-warp regions (alias s_hist once the HUGE phase is over):
-  // 256 histogram bins + a 64-entry active list
-  uint32_t* w_bins = s_hist + (WARP_BINS + 64) * warp_id();
-  uint32_t* w_list = w_bins + WARP_BINS;
+  // per-warp histogram bins (alias s_hist once the HUGE phase is over)
+  uint32_t* w_bins = s_hist + WARP_BINS * warp_id();
   __shared__ uint32_t s_red[33];
   __shared__ uint32_t s_item;
   __shared__ uint32_t s_drop;
-  __shared__ unsigned long long s_acc[4];
+  __shared__ unsigned long long s_acc[5];
   const uint32_t tid = threadIdx.x;
-  const uint32_t gtid = blockIdx.x * blockDim.x + tid;
-  const uint32_t gsize = gridDim.x * blockDim.x;
-  const bool snapshot = p.rule >= R_SNAP_EXT;
+  const bool count = p.rule == R_COUNT;
 
   for (uint32_t r = p.r_begin; r < p.r_end; ++r) {
     const uint32_t cur = r & 1, nxt = cur ^ 1;
     const uint32_t sr = r < STAT_SLOTS - 1 ? r : STAT_SLOTS - 1;
     RoundView<EstT> rv;
-    rv.snap = snapshot ? p.est[cur] : p.est[0];
-    rv.next = p.est[nxt];
-    rv.fcur = p.flag[cur];
+    rv.snap = p.E;
     rv.fnxt = p.flag[nxt];
+    rv.qcnt = p.ctl[cur].qcnt;
     rv.grab = p.ctl[cur].grab;
-    rv.snapshot = snapshot;
-    rv.ext = p.rule == R_SNAP_EXT || p.rule == R_REF_EXT;
+    rv.count = count;
+    rv.ext = p.rule != R_REF_PLAIN;
+    rv.skip_a = count && r > 0;
     unsigned long long* pf = (p.prof && r < PROF_ROUNDS && tid == 0)
                                  ? p.prof + ((size_t)r * gridDim.x + blockIdx.x) * PROF_PHASES
                                  : nullptr;
     if (pf) pf[0] = gtimer();
-    // cursors and drop flag of the NEXT round (nobody touches them now)
-    if (blockIdx.x == 0 && tid < NCLS + 2) p.ctl[nxt].grab[tid] = 0;
-    if (blockIdx.x == 0 && tid == 32) p.anydrop[(r + 1) % 3] = 0;
-    if (p.cache_n) {
-      // vectorised cache fill: cache_n * sizeof(EstT) is a multiple of 16 bytes
-      const uint4* src = reinterpret_cast<const uint4*>(rv.snap);
-      uint4* dst = reinterpret_cast<uint4*>(s_cache);
-      const uint32_t nvec = (uint32_t)((size_t)p.cache_n * sizeof(EstT) / 16);
-      for (uint32_t i = tid; i < nvec; i += SOLVE_THREADS) dst[i] = src[i];
+    // cursors, queue counts and drop flag of the NEXT round (idle now)
+    if (blockIdx.x == 0 && tid < NCLS) {
+      p.ctl[nxt].grab[tid] = 0;
+      p.ctl[nxt].grab2[tid] = 0;
+      p.ctl[nxt].qcnt[tid] = 0;
     }
-    if (tid < 4) s_acc[tid] = 0;
+    if (blockIdx.x == 0 && tid == 32) p.anydrop[(r + 1) % 3] = 0;
+    // ---------------- COMPACT round r's flags ----------------
+    compact_frontier(p, p.flag[cur], p.ctl[cur].qcnt, s_red, &s_item);
+    if (tid < 5) s_acc[tid] = 0;
     if (tid == 0) s_drop = 0;
+    grid.sync();
+    // the shared-memory cache pays off only when the round has real work
+    uint32_t active = 0;
+#pragma unroll
+    for (int c = 0; c < NCLS; ++c) active += rv.qcnt[c];
+    const uint32_t cache_n = active >= CACHE_MIN_ACTIVE ? p.cache_n : 0u;
+    rv.cache_n = cache_n;
+    if (cache_n) fill_cache(s_cache, (const EstT*)p.E, cache_n);
     __syncthreads();
-    Acc acc{0, 0, 0, 0, false};
+    Acc acc{0, 0, 0, 0, 0, false};
     if (pf) pf[1] = gtimer();
+    // ---------------- EVALUATE ----------------
     eval_huge(p, rv, s_cache, s_hist, s_red, &s_item, acc);
     if (pf) pf[2] = gtimer();
-    eval_wstream<CH_BIG>(p, rv, s_cache, C_BIG, w_bins, w_list, acc);
+    eval_wstream<G_BIG>(p, rv, s_cache, C_BIG, w_bins, acc);
+    eval_wstream<G_WARP>(p, rv, s_cache, C_WARP, w_bins, acc);
     if (pf) pf[3] = gtimer();
-    eval_wstream<CH_WARP>(p, rv, s_cache, C_WARP, w_bins, w_list, acc);
+    eval_sub(p, rv, s_cache, acc);
+    eval_thread(p, rv, s_cache, acc);
     if (pf) pf[4] = gtimer();
-    eval_sub(p, rv, s_cache, w_list, acc);
-    if (pf) pf[5] = gtimer();
-    eval_thread(p, rv, s_cache, w_list, acc);
-    if (pf) pf[6] = gtimer();
     if (__any_sync(FULL, acc.any_drop) && lane_id() == 0) s_drop = 1;
-    flush_acc(p, sr, acc, s_acc);  // contains __syncthreads
+    __syncthreads();
     if (tid == 0 && s_drop) p.anydrop[r % 3] = 1;
     grid.sync();
-    const bool any = *reinterpret_cast<volatile uint32_t*>(&p.anydrop[r % 3]) != 0;
+    // The reference starts at est = deg (fastk.cpp:67-68); the solver starts
+    // at min(deg, H), so round 0 "changed" also when some degree exceeds H
+    // (that drop is already applied).  Keeps iterations equal to the reference.
+    const bool any = *reinterpret_cast<volatile uint32_t*>(&p.anydrop[r % 3]) != 0 ||
+                     (r == 0 && p.clamp_drop);
     if (!any) {  // quiescent round: converged (fastk.cpp:109-110)
+      flush_acc(p, sr, acc, s_acc);
       if (blockIdx.x == 0 && tid == 0) {
         p.status[0] = r + 1;
         p.status[1] = 1;
-        p.status[3] = snapshot ? cur : 0;
+        p.status[3] = 0;
       }
-      if (pf) pf[7] = gtimer();
+      if (pf) pf[5] = pf[6] = pf[7] = gtimer();
       return;
     }
-    if (!snapshot) {
-      // apply (fastk.cpp:153): est[u] = new value for every dropper
-      const uint32_t nw = (p.n_nz + 3) / 4;
-      for (uint32_t w = gtid; w < nw; w += gsize) {
-        const uint32_t m = reinterpret_cast<const uint32_t*>(p.dropped)[w];
-        if (!m) continue;
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-          if (m >> (8 * b) & 0xffu) p.est[0][4 * w + b] = p.est[1][4 * w + b];
-      }
-      grid.sync();
-      if (tid < 4) s_acc[tid] = 0;
-      __syncthreads();
-      Acc nacc{0, 0, 0, 0, false};
-      notify_settled(p, rv, w_list, nacc);
-      flush_acc(p, sr, nacc, s_acc);
-      grid.sync();
-    }
+    if (pf) pf[5] = gtimer();
+    // ---------------- NOTIFY + APPLY ----------------
+    rv.snap = p.N;
+    rv.grab = p.ctl[cur].grab2;
+    if (cache_n) fill_cache(s_cache, (const EstT*)p.N, cache_n);
+    __syncthreads();
+    if (pf) pf[6] = gtimer();
+    notify_huge(p, rv, s_cache, &s_item, acc);
+    notify_wstream<G_BIG>(p, rv, s_cache, C_BIG, acc);
+    notify_wstream<G_WARP>(p, rv, s_cache, C_WARP, acc);
+    notify_small<G_SUB>(p, rv, s_cache, C_SUB, acc);
+    notify_small<G_THREAD>(p, rv, s_cache, C_THREAD, acc);
+    flush_acc(p, sr, acc, s_acc);
+    grid.sync();
     if (pf) pf[7] = gtimer();
     if (blockIdx.x == 0 && tid == 0) {
       p.status[0] = r + 1;
-      p.status[3] = snapshot ? nxt : 0;
+      p.status[3] = 0;
     }
   }
 }
 
-// Round-0 state: est = min(deg, H) in both buffers (identical
-// trajectory from round 1; the reference starts at deg, fastk.cpp:67-68),
-// every non-isolated vertex flagged active, everything else cleared.
+// Round-0 state: E = N = min(deg, H) (identical trajectory
+// from round 1; the reference starts at deg, fastk.cpp:67-68), every
+// non-isolated vertex active, everything else cleared.
 template <typename OffT, typename EstT>
 __global__ void init_kernel(P<OffT, EstT> p, uint32_t h_graph, uint32_t n_pad) {
   const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -850,17 +958,17 @@ __global__ void init_kernel(P<OffT, EstT> p, uint32_t h_graph, uint32_t n_pad) {
       const uint32_t d = (uint32_t)(p.off[u + 1] - p.off[u]);
       e = (EstT)(d < h_graph ? d : h_graph);
     }
-    p.est[0][u] = e;
-    p.est[1][u] = e;
+    p.E[u] = e;
+    p.N[u] = e;
+    p.cnt[u] = 0;
     p.flag[0][u] = u < p.n_nz ? 1 : 0;
     p.flag[1][u] = 0;
-    p.dropped[u] = 0;
   }
   for (uint32_t k = gtid; k < STAT_SLOTS * (uint32_t)(sizeof(RoundStat) / 8); k += gsize)
     reinterpret_cast<unsigned long long*>(p.stats)[k] = 0;
-  if (gtid < NCLS + 2) {
-    p.ctl[0].grab[gtid] = 0;
-    p.ctl[1].grab[gtid] = 0;
+  if (gtid < NCLS) {
+    p.ctl[0].grab[gtid] = p.ctl[0].grab2[gtid] = p.ctl[0].qcnt[gtid] = 0;
+    p.ctl[1].grab[gtid] = p.ctl[1].grab2[gtid] = p.ctl[1].qcnt[gtid] = 0;
   }
   if (gtid < 3) p.anydrop[gtid] = 0;
   if (gtid < 4) p.status[gtid] = 0;
@@ -873,12 +981,12 @@ P<OffT, EstT> make_params(const SolveBuffers& b) {
   p.adj = b.adj;
   p.n_nz = b.n_nz;
   for (int c = 0; c <= NCLS; ++c) p.cb[c] = b.cls_begin[c];
-  p.est[0] = static_cast<EstT*>(b.est[0]);
-  p.est[1] = static_cast<EstT*>(b.est[1]);
-  p.old = static_cast<EstT*>(b.old);
+  p.E = static_cast<EstT*>(b.est[0]);
+  p.N = static_cast<EstT*>(b.est[1]);
+  p.cnt = b.cnt;
   p.flag[0] = b.flag[0];
   p.flag[1] = b.flag[1];
-  p.dropped = b.dropped;
+  p.queue = b.queue;
   p.ctl = b.ctl;
   p.anydrop = b.anydrop;
   p.stats = b.stats;
@@ -895,7 +1003,8 @@ cudaError_t launch_rounds_t(const SolveBuffers& b, const SolveConfig& c, uint32_
   p.r_end = r_end;
   p.rule = c.rule;
   p.cache_n = c.cache_n;
-  const size_t warp_region = (size_t)32 * (WARP_BINS + 64);
+  p.clamp_drop = c.clamp_drop;
+  const size_t warp_region = (size_t)NWARPS * WARP_BINS;
   const size_t hist = (size_t)HIST_BINS > warp_region ? (size_t)HIST_BINS : warp_region;
   const size_t smem = (((size_t)c.cache_n * sizeof(EstT) + 15) & ~(size_t)15) +
                       hist * sizeof(uint32_t);
@@ -922,9 +1031,13 @@ cudaError_t launch_init_t(const SolveBuffers& b, uint32_t h_graph, cudaStream_t 
 }  // namespace
 
 size_t solver_cache_bytes_max() {
-  // 227 KB opt-in per CTA: 128 KB of estimates + 40 KB of per-warp bins and
-  // lists; the rest stays L1 for the estimate gathers.
+  // 227 KB opt-in per CTA: 128 KB of estimates + the histogram / per-warp
+  // regions; the rest stays L1 for the estimate gathers.
+#ifdef KC_CACHE_KB
+  return KC_CACHE_KB * 1024;
+#else
   return 128 * 1024;
+#endif
 }
 
 cudaError_t launch_rounds(const SolveBuffers& b, const SolveConfig& c, bool est16, bool off64,

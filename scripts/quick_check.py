@@ -5,7 +5,7 @@ sys.path.insert(0, "/root/repo")
 from oracle import pyoracle as O
 import paper_2512_00233_b200 as K
 
-def check(name, n, pairs, rules=(K.Rule.SNAPSHOT, K.Rule.REFERENCE)):
+def check(name, n, pairs, rules=(K.Rule.COUNTING, K.Rule.REFERENCE)):
     g = O.build_csr(n, pairs)
     truth = O.peel(g)
     G = K.Graph(g.off, g.nbr)
@@ -36,4 +36,4 @@ check("rmat12", 1<<12, O.gen_rmat(12, 16, 3))
 check("rmat16", 1<<16, O.gen_rmat(16, 16, 3))
 check("cl1e5", 100000, O.gen_chunglu(100000, 4, cliques=5, csize=100))
 check("er100k", 100000, O.gen_er(100000, 1000000, 1))
-check("rmat20", 1<<20, O.gen_rmat(20, 16, 3), rules=(K.Rule.SNAPSHOT,))
+check("rmat20", 1<<20, O.gen_rmat(20, 16, 3), rules=(K.Rule.COUNTING,))

@@ -1,0 +1,54 @@
+"""Host-side mirror of the reference API (paper_2512_00233_b200.api) on CPU:
+graph construction, result aggregates, rules — against the oracle, the
+reference and the golden fixtures."""
+import numpy as np
+
+from conftest import golden
+
+
+def test_graph_from_edges_matches_reference_builder(kc, ref):
+    rng = np.random.default_rng(3)
+    for _ in range(15):
+        n = int(rng.integers(1, 200))
+        pairs = rng.integers(0, n, (int(rng.integers(0, 800)), 2))
+        g = kc.Graph.from_edges(n, pairs.tolist())
+        r = ref.RefGraph(n=n, pairs=pairs.astype(np.uint32).reshape(-1)).csr()
+        assert np.array_equal(g.offsets(), r.off)
+        assert np.array_equal(g.neighbor_array(), r.nbr)
+        assert g.node_count() == n
+        assert g.edge_count() == r.nbr.size // 2
+
+
+def test_graph_accessors():
+    import paper_2512_00233_b200 as K
+    g = K.Graph.from_edges(5, [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3), (3, 4), (4, 4)])
+    assert g.degree(3) == 4 and list(g.neighbors(3)) == [0, 1, 2, 4]
+    assert g.edge_count() == 7
+    e = K.Graph()
+    assert e.node_count() == 0 and e.edge_count() == 0
+
+
+def test_make_coreness_result():
+    import paper_2512_00233_b200 as K
+    # tests/test_oracle.cpp:79-87
+    r = K.make_coreness_result([3, 1, 2])
+    assert r.k_max == 3 and abs(r.k_avg - 2.0) < 1e-12
+    e = K.make_coreness_result([])
+    assert e.k_max == 0 and e.k_avg == 0.0
+
+
+def test_rule_helpers_match_reference():
+    import paper_2512_00233_b200 as K
+    g = golden("rules.json")
+    for c in g["should_notify"]:
+        assert int(K.should_notify(*c["args"])) == c["value"]
+    for c in g["switch_condition"]:
+        assert int(K.switch_condition(*c["args"])) == c["value"]
+
+
+def test_named_graph_fixtures_roundtrip():
+    import paper_2512_00233_b200 as K
+    for name, g in golden("named_graphs.json").items():
+        G = K.Graph.from_edges(g["n"], g["edges"])
+        assert G.offsets().tolist() == g["offsets"], name
+        assert G.neighbor_array().tolist() == g["neighbors"], name
