@@ -110,6 +110,16 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def reduce_max(value: float, dist, device="cuda"):
+    """Max over ranks (timings are the slowest rank's); identity without dist."""
+    if dist is None or not dist.is_initialized():
+        return float(value)
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -174,11 +184,7 @@ def run_ours(args, ws, rank, local):
     if dist:
         dist.barrier()
     ms = [s["t_solve_ms"] for s in stats]
-    ms_step = sum(ms) / len(ms)
-    if dist:
-        tt = torch.tensor([ms_step], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_step = float(tt.item())
+    ms_step = reduce_max(sum(ms) / len(ms), dist, device=f"cuda:{local}")
     st = stats[-1]
     e_ref, e_our, v_our = st_ref["e_scan"], st["e_scan"], st["v_eval"]
     gteps = ws * e_ref / (ms_step * 1e-3) / 1e9
@@ -199,11 +205,7 @@ def run_ours(args, ws, rank, local):
         g2.free()
         if i:  # first call warms up
             e2e_ms.append((time.perf_counter() - t) * 1e3)
-    e2e_ms_step = sum(e2e_ms) / len(e2e_ms)
-    if dist:
-        tt = torch.tensor([e2e_ms_step], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms_step = float(tt.item())
+    e2e_ms_step = reduce_max(sum(e2e_ms) / len(e2e_ms), dist, device=f"cuda:{local}")
 
     peak, peak_src = measured_peak()
     bytes_alg = 8 * e_our + 16 * v_our

@@ -1,0 +1,320 @@
+"""Parity of the sm_100a path (C-ABI, libkcore_b200.so) with the reference.
+
+Every GPU result is compared bit-exactly with the oracle's peel
+(kcore::peel_coreness restated, pinned in test_oracle.py) or with golden
+fixtures produced by the reference itself.  Mirrors tests/test_fastk.cpp and
+tests/acceptance.cpp criterion 1 of the reference.
+"""
+import hashlib
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden
+
+pytestmark = pytest.mark.gpu
+
+RULES = ("REFERENCE", "COUNTING")
+
+
+def union_csr(oracle, graphs):
+    """Disjoint union of (n, edges) graphs — coreness is per component."""
+    base = 0
+    chunks = []
+    for n, edges in graphs:
+        e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+        if e.size:
+            chunks.append((e + base).astype(np.uint32))
+        base += n
+    pairs = np.concatenate(chunks).reshape(-1) if chunks else np.zeros(0, np.uint32)
+    return oracle.build_csr(base, pairs)
+
+
+def to_graph(kc, csr):
+    return kc.Graph(csr.off, csr.nbr)
+
+
+def solve(kc, g, rule="COUNTING", **kw):
+    r = kc.fastk_run(g, kc.FastKOptions(rule=kc.Rule[rule], **kw))
+    return r.result.coreness, r
+
+
+# ---------------------------------------------------------------- fixtures
+def test_named_graphs_and_reference_counters(gpu, oracle):
+    for name, g in golden("named_graphs.json").items():
+        G = gpu.Graph(np.array(g["offsets"], np.uint64), np.array(g["neighbors"], np.uint32))
+        for rule in RULES:
+            core, r = solve(gpu, G, rule)
+            assert core.tolist() == g["coreness"], (name, rule)
+            assert r.result.k_max == g["k_max"]
+            assert abs(r.result.k_avg - g["k_avg"]) < 1e-9
+        for ext in (True, False):
+            # RunReport equality with the reference (hybrid tail off)
+            want = g["fastk"][f"ext{int(ext)}_tail0_b256"]
+            _, r = solve(gpu, G, "REFERENCE", extended_notify=ext, hybrid_tail=False)
+            got = {k: getattr(r.report, k) for k in want}
+            assert got == want, (name, ext)
+
+
+def test_empty_and_edgeless(gpu):
+    # tests/test_fastk.cpp:156-164
+    r = gpu.fastk_run(gpu.Graph(), gpu.FastKOptions(threads=3, batch=8))
+    assert r.result.coreness.size == 0 and r.report.iterations == 1
+    lone = gpu.Graph.from_edges(4, [])
+    r = gpu.fastk_run(lone, gpu.FastKOptions(threads=2, batch=2))
+    assert r.result.coreness.tolist() == [0, 0, 0, 0]
+    assert r.report.messages_sent == 0
+    one = gpu.Graph.from_edges(1, [])
+    assert gpu.fastk_run(one).result.coreness.tolist() == [0]
+
+
+def test_random_graphs_golden(gpu):
+    for g in golden("random_graphs.json"):
+        G = gpu.Graph.from_edges(g["n"], g["edges"])
+        for rule in RULES:
+            core, _ = solve(gpu, G, rule)
+            assert core.tolist() == g["coreness"], rule
+        for ext in (True, False):
+            want = g["fastk"][f"ext{int(ext)}_tail0_b3"]
+            _, r = solve(gpu, G, "REFERENCE", extended_notify=ext, hybrid_tail=False)
+            assert {k: getattr(r.report, k) for k in want} == want
+
+
+def test_no_lost_updates_trajectory(gpu):
+    """tests/test_fastk.cpp:232-266: per-iteration snapshots and active counts
+    equal the reference's (shadow_run) evolution."""
+    n_checked = 0
+    for g in golden("random_graphs.json"):
+        if "observed" not in g:
+            continue
+        G = gpu.Graph.from_edges(g["n"], g["edges"])
+        for ext in (1, 0):
+            want = g["observed"][f"ext{ext}"]
+            snaps, acts = [], []
+            instr = gpu.Instrumentation(inspector=lambda it, est, a: (snaps.append(est.tolist()),
+                                                                      acts.append(a)))
+            r = gpu.fastk_run(G, gpu.FastKOptions(rule=gpu.Rule.REFERENCE,
+                                                  extended_notify=bool(ext), hybrid_tail=False),
+                              instr)
+            assert snaps == want["snapshots"]
+            assert acts == want["active"]
+            assert r.report.iterations == want["report"]["iterations"]
+            assert r.report.messages_sent == want["report"]["messages_sent"]
+            assert r.report.messages_drained == want["report"]["messages_drained"]
+            # the counting rule follows the same estimate trajectory
+            snaps2 = []
+            instr2 = gpu.Instrumentation(inspector=lambda it, est, a: snaps2.append(est.tolist()))
+            gpu.fastk_run(G, gpu.FastKOptions(rule=gpu.Rule.COUNTING), instr2)
+            assert snaps2 == want["snapshots"]
+            n_checked += 1
+    assert n_checked >= 8
+
+
+def test_sound_monotone_zero_activity(gpu, oracle):
+    # tests/test_fastk.cpp:268-288
+    rng = np.random.default_rng(411)
+    n = 80
+    edges = [(i, j) for i in range(n) for j in range(i + 1, n) if rng.random() < 0.08]
+    G = gpu.Graph.from_edges(n, edges)
+    truth = oracle.peel(oracle.csr_from_edges(n, edges))
+    for rule in RULES:
+        snaps, acts = [], []
+        gpu.fastk_run(G, gpu.FastKOptions(rule=gpu.Rule[rule]),
+                      gpu.Instrumentation(inspector=lambda it, e, a: (snaps.append(e.copy()),
+                                                                     acts.append(a))))
+        assert np.array_equal(snaps[0], G.degrees())
+        for i in range(1, len(snaps)):
+            assert (snaps[i] <= snaps[i - 1]).all() and (snaps[i] >= truth).all()
+        assert np.array_equal(snaps[-1], truth)
+        assert acts[0] == n and acts[-1] == 0
+
+
+def test_convergence_trace_star4(gpu):
+    """tests/test_bench.cpp:166-176 (kcbench trace, FastK): rows
+    0,0.6,1.0 / 1,0,0 / 2,0,0."""
+    want = golden("trace_star4.json")
+    G = gpu.Graph.from_edges(5, [(0, 1), (0, 2), (0, 3), (0, 4)])
+    truth = gpu.make_coreness_result([1, 1, 1, 1, 1])
+    for rule in RULES:
+        r = gpu.fastk_run(G, gpu.FastKOptions(rule=gpu.Rule[rule]),
+                          gpu.Instrumentation(truth=truth, trace_convergence=True))
+        assert [round(t.mean_error, 6) for t in r.report.trace] == want["mean_error"]
+        assert [round(t.active_fraction, 6) for t in r.report.trace] == want["active_fraction"]
+
+
+# ---------------------------------------------------------------- exhaustive
+def labeled_union(n_max):
+    graphs = []
+    for n in range(1, n_max + 1):
+        pairs = list(itertools.combinations(range(n), 2))
+        m = len(pairs)
+        masks = np.arange(1 << m, dtype=np.int64)
+        cnt = masks.size
+        base = np.arange(cnt, dtype=np.int64) * n
+        e_all = []
+        for b, (i, j) in enumerate(pairs):
+            sel = (masks >> b) & 1 == 1
+            e_all.append(np.stack([base[sel] + i, base[sel] + j], 1))
+        graphs.append((cnt * n, np.concatenate(e_all) if e_all else np.zeros((0, 2), np.int64)))
+    return graphs
+
+
+@pytest.mark.parametrize("n_max", [6, 7])
+def test_every_labeled_graph_as_one_union(gpu, oracle, n_max):
+    """Every labeled graph on <= n_max nodes (2^21 graphs for 7 nodes) in one
+    disjoint-union call: a superset of acceptance.cpp criterion 1's unlabeled
+    <= 8-node sweep for n <= 7."""
+    g = union_csr(oracle, labeled_union(n_max))
+    truth = oracle.peel(g)
+    for rule in RULES:
+        core, _ = solve(gpu, to_graph(gpu, g), rule)
+        assert np.array_equal(core, truth), rule
+
+
+def test_random_8_node_and_gnp_unions(gpu, oracle):
+    # acceptance.cpp:267-270: 1000 G(n, p), n in [2, 64], p in [0.01, 0.5]
+    rng = np.random.default_rng(909)
+    graphs = []
+    for _ in range(1000):
+        n = int(rng.integers(2, 65))
+        p = rng.uniform(0.01, 0.5)
+        iu = np.triu_indices(n, 1)
+        keep = rng.random(iu[0].size) < p
+        graphs.append((n, np.stack([iu[0][keep], iu[1][keep]], 1)))
+    for _ in range(3000):  # random 8-node graphs
+        iu = np.triu_indices(8, 1)
+        keep = rng.random(28) < rng.uniform(0.1, 0.9)
+        graphs.append((8, np.stack([iu[0][keep], iu[1][keep]], 1)))
+    g = union_csr(oracle, graphs)
+    truth = oracle.peel(g)
+    for rule in RULES:
+        for ext in (True, False):
+            core, _ = solve(gpu, to_graph(gpu, g), rule, extended_notify=ext)
+            assert np.array_equal(core, truth)
+
+
+def test_bit_identical_across_options_and_repeats(gpu, oracle):
+    # tests/test_fastk.cpp:205-230
+    g = to_graph(gpu, oracle.build_csr(5000, oracle.gen_er(5000, 40000, 405)))
+    base, _ = solve(gpu, g)
+    for t, b in itertools.product((1, 4, 16), (1, 64, 4096)):
+        core, _ = solve(gpu, g, threads=t, batch=b)
+        assert np.array_equal(core, base)
+    gg = gpu.GpuGraph(g)
+    for _ in range(5):
+        core, st = gg.solve(gpu.FastKOptions())
+        assert np.array_equal(core, base)
+
+
+def test_plain_guard_notifies_at_least_as_often(gpu):
+    # tests/test_fastk.cpp:290-301
+    rng = np.random.default_rng(413)
+    for _ in range(4):
+        n = 100
+        edges = [(i, j) for i in range(n) for j in range(i + 1, n) if rng.random() < 0.06]
+        G = gpu.Graph.from_edges(n, edges)
+        _, ext = solve(gpu, G, "REFERENCE", extended_notify=True, hybrid_tail=False)
+        _, plain = solve(gpu, G, "REFERENCE", extended_notify=False, hybrid_tail=False)
+        assert ext.result.coreness.tolist() == plain.result.coreness.tolist()
+        assert ext.report.messages_sent <= plain.report.messages_sent
+        assert ext.report.messages_drained <= plain.report.messages_drained
+        assert ext.report.iterations == plain.report.iterations
+
+
+def test_long_path_many_rounds(gpu):
+    """A path needs ~n/2 Jacobi rounds; no round cap may cut it short."""
+    n = 3001
+    G = gpu.Graph.from_edges(n, [(i, i + 1) for i in range(n - 1)])
+    for rule in RULES:
+        core, r = solve(gpu, G, rule)
+        assert (core == 1).all()
+        assert r.report.iterations >= n // 2 - 2
+
+
+# ---------------------------------------------------------------- layouts
+@pytest.mark.parametrize("flags", [0, 1, 2, 3])
+def test_layout_variants(gpu, oracle, flags):
+    """All four kernel instantiations (uint32/uint64 offsets x uint16/uint32
+    estimates) give the same coreness."""
+    g = oracle.build_csr(1 << 14, oracle.gen_rmat(14, 16, 7))
+    truth = oracle.peel(g)
+    gg = gpu.GpuGraph(to_graph(gpu, g), flags=flags)
+    for rule in RULES:
+        core, _ = gg.solve(gpu.FastKOptions(rule=gpu.Rule[rule]))
+        assert np.array_equal(core, truth)
+
+
+@pytest.mark.parametrize("cache", [0, 0xFFFFFFFF, 1024])
+def test_smem_cache_setting_is_invisible(gpu, oracle, cache):
+    g = oracle.build_csr(1 << 15, oracle.gen_rmat(15, 16, 9))
+    truth = oracle.peel(g)
+    core, _ = solve(gpu, to_graph(gpu, g), smem_cache=cache)
+    assert np.array_equal(core, truth)
+
+
+# ---------------------------------------------------------------- configs
+def small_configs(oracle):
+    yield "er", 100000, oracle.gen_er(100000, 1000000, 1)
+    yield "grid", 512 * 512, oracle.gen_grid(512, 2)
+    yield "rmat16", 1 << 16, oracle.gen_rmat(16, 16, 3)
+    yield "chunglu", 200000, oracle.gen_chunglu(200000, 4, cliques=10, csize=100)
+    yield "rmat18", 1 << 18, oracle.gen_rmat(18, 16, 5)
+
+
+def test_scaled_configs_vs_oracle(gpu, oracle):
+    for name, n, pairs in small_configs(oracle):
+        g = oracle.build_csr(n, pairs)
+        truth = oracle.peel(g)
+        for rule in RULES:
+            core, r = solve(gpu, to_graph(gpu, g), rule)
+            assert np.array_equal(core, truth), (name, rule)
+            assert r.result.k_max == int(truth.max())
+
+
+def _digests():
+    path = os.path.join(ROOT, "tests", "golden", "configs.json")
+    return json.load(open(path)) if os.path.exists(path) else {}
+
+
+CFG = {1: (100000, 1000000, 0, 1), 2: (4096, 0, 0, 2), 3: (22, 16, 0, 3),
+       4: (20000000, 200, 300, 4), 5: (26, 16, 0, 5)}
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, pytest.param(4, marks=pytest.mark.slow),
+                                 pytest.param(5, marks=pytest.mark.slow)])
+def test_full_size_configs_vs_golden(gpu, cfg):
+    """BASELINE.json configs at full size, built in HBM by the kcgen v1
+    generator: CSR digest and coreness digest equal the oracle's (computed
+    from the CPU generator + kcore::peel_coreness restated)."""
+    d = _digests().get(str(cfg))
+    if d is None:
+        pytest.skip(f"golden digest for config {cfg} not generated")
+    p0, p1, p2, seed = CFG[cfg]
+    dcsr = gpu.gen_config(cfg, p0, p1, p2, seed=seed)
+    assert (dcsr.n, dcsr.nnz) == (d["n"], d["nnz"])
+    host = dcsr.download()
+    assert hashlib.sha256(host.offsets().tobytes()).hexdigest() == d["offsets_sha256"]
+    assert hashlib.sha256(host.neighbor_array().tobytes()).hexdigest() == d["neighbors_sha256"]
+    gg = gpu.GpuGraph(dcsr)
+    core, st = gg.solve(gpu.FastKOptions())
+    assert hashlib.sha256(core.astype(np.uint32).tobytes()).hexdigest() == d["coreness_sha256"]
+    assert st["k_max"] == d["k_max"] and st["h_graph"] == d["h_graph"]
+    if "jacobi_ref_ext" in d:  # reference rule: exact RunReport vs the CPU replay
+        core2, st2 = gg.solve(gpu.FastKOptions(rule=gpu.Rule.REFERENCE, hybrid_tail=False))
+        assert np.array_equal(core, core2)
+        j = d["jacobi_ref_ext"]
+        assert st2["iterations"] == j["iterations"]
+        assert st2["messages_sent"] == j["messages_sent"]
+        assert st2["e_scan"] == j["e_scan"]
+
+
+def test_invalid_arguments_on_device(gpu):
+    g = gpu.Graph.from_edges(3, [(0, 1), (1, 2), (0, 2)])
+    with pytest.raises(ValueError):
+        gpu.fastk_run(g, gpu.FastKOptions(threads=0))
+    gg = gpu.GpuGraph(g)
+    with pytest.raises(ValueError):
+        gg.solve(gpu.FastKOptions(batch=0))
