@@ -1,0 +1,88 @@
+// kcore_gpu.cpp — see kcore_gpu.hpp.  Host-side adapter over the C-ABI.
+#include "kcore_gpu.hpp"
+
+#include <cstring>
+#include <new>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kcore/oracle.hpp"
+#include "kcore_b200.h"
+
+namespace kcore::gpu {
+
+namespace {
+
+[[noreturn]] void raise(kc_status s, const char* where) {
+  const std::string msg = std::string(where) + ": " + kc_status_str(s) + " (" + kc_last_error() + ")";
+  if (s == KC_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (s == KC_ERR_OUT_OF_MEMORY) throw std::bad_alloc();
+  throw std::runtime_error(msg);
+}
+
+struct HookCtx {
+  RunReport* report;
+  const Instrumentation* instr;
+};
+
+// Engines call instrument_boundary (report.cpp:20-29) at every boundary;
+// the C-ABI inspector delivers exactly those boundaries.
+int on_boundary(void* user, uint64_t iteration, const uint32_t* est, uint32_t n,
+                uint64_t active) {
+  auto* c = static_cast<HookCtx*>(user);
+  instrument_boundary(*c->report, c->instr, iteration, std::span<const uint32_t>(est, n), active);
+  return 0;
+}
+
+}  // namespace
+
+EngineResult fastk_run(const Graph& g, const FastKOptions& opt, const Instrumentation* instr,
+                       Rule rule) {
+  if (opt.threads == 0) throw std::invalid_argument("fastk: threads must be >= 1");
+  if (opt.batch == 0) throw std::invalid_argument("fastk: batch must be >= 1");
+
+  const uint32_t n = g.node_count();
+  kc_csr_view view{};
+  view.n = n;
+  view.nnz = g.offsets().back();
+  view.offsets = g.offsets().data();
+  // neighbors(0) is only valid when n > 0 (offsets_ == {0} for the empty graph)
+  view.neighbors = (n > 0 && view.nnz > 0) ? g.neighbors(0).data() : nullptr;
+
+  kc_options o;
+  kc_default_options(&o);
+  o.threads = opt.threads;
+  o.batch = opt.batch;
+  o.extended_notify = opt.extended_notify ? 1 : 0;
+  o.hybrid_tail = opt.hybrid_tail ? 1 : 0;
+  o.rule = static_cast<int32_t>(rule);
+
+  EngineResult out;
+  std::vector<uint32_t> core(n);
+  kc_stats st{};
+  kc_graph* h = nullptr;
+  kc_status s = kc_graph_upload(&view, 0, &h);
+  if (s != KC_OK) raise(s, "kc_graph_upload");
+  const bool observed = instr && (instr->trace_convergence || instr->inspector);
+  if (observed) {
+    HookCtx ctx{&out.report, instr};
+    s = kc_solve_observed(h, &o, &on_boundary, &ctx, core.data(), &st);
+  } else {
+    s = kc_solve(h, &o, core.data(), &st);
+  }
+  kc_graph_free(h);
+  if (s != KC_OK) raise(s, "kc_solve");
+
+  out.report.iterations = st.iterations;
+  out.report.messages_sent = st.messages_sent;
+  out.report.messages_drained = st.messages_drained;
+  out.report.tail_pops = st.tail_pops;
+  out.result.coreness = std::move(core);
+  out.result.k_max = st.k_max;
+  out.result.k_avg = st.k_avg;
+  return out;
+}
+
+}  // namespace kcore::gpu
