@@ -55,59 +55,84 @@ def dist_env():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """SM clock + throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line) — NVML every 5 ms on a thread; falls
+    back to `nvidia-smi -lms 100` when NVML is unavailable."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {  # nvmlClocksEventReason* bits
+        "hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+        "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80,
+    }
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
-            self._t.start()
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        if self._nvml is None:
+            return self._run_smi()
+        N = self._nvml
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self._h, N.NVML_CLOCK_SM))
+                bits = N.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, b in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.005)
+
+    def _run_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits", "-lms", "100"],
+                                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            return
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in p.stdout:
+            f = [x.strip() for x in line.split(",")]
+            try:
+                self.samples.append(float(f[0]))
+                self.max_mhz = float(f[1])
+            except (ValueError, IndexError):
+                pass
+            for nm, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    self.reasons.add(nm)
+            if self._stop.is_set():
+                break
+        p.terminate()
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-            self._t.join(timeout=2)
+        self._stop.set()
+        self._t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def reduce_max(value: float, dist, device="cuda"):
@@ -197,14 +222,16 @@ def run_ours(args, ws, rank, local):
     core_p = torch.empty(max(n, 1), dtype=torch.int32).pin_memory()
     core_np = core_p.numpy().view(np.uint32)
     e2e_steps = max(1, min(args.steps, 5))
-    e2e_ms = []
+    e2e_ms, parts = [], []
     for i in range(e2e_steps + 1):
         t = time.perf_counter()
         g2 = K.GpuGraph(pinned, device=local)
-        g2.solve(opts, out=core_np)
+        _, st2 = g2.solve(opts, out=core_np)
         g2.free()
         if i:  # first call warms up
             e2e_ms.append((time.perf_counter() - t) * 1e3)
+            parts.append({k: st2[k] for k in ("t_upload_ms", "t_prep_ms", "t_solve_ms",
+                                              "t_download_ms")})
     e2e_ms_step = reduce_max(sum(e2e_ms) / len(e2e_ms), dist, device=f"cuda:{local}")
 
     peak, peak_src = measured_peak()
@@ -214,7 +241,7 @@ def run_ours(args, ws, rank, local):
     line = {
         "metric": METRIC, "value": round(gteps, 3), "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16/u32",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16" if st["h_graph"] < 32768 else "u32",
         "data": "synthetic (kcgen v1 seeded generator, built in HBM)",
         "config": {"workload": f"cfg{args.config}: {desc}", "n": n, "nnz": nnz,
                    "parallelism": f"replicas{ws}" if ws > 1 else "single GPU",
@@ -233,6 +260,7 @@ def run_ours(args, ws, rank, local):
         "e2e": {"value": round(ws * e_ref / (e2e_ms_step * 1e-3) / 1e9, 3), "unit": UNIT,
                 "ms_per_step": round(e2e_ms_step, 3),
                 "h2d_bytes_per_step": int((n + 1) * 8 + nnz * 4),
+                "device_ms": {k: round(statistics.mean(p[k] for p in parts), 3) for k in parts[0]},
                 "d2h_bytes_per_step": int(n * 4)},
         "gpu_launches": 4 * args.steps,
         "clocks": clk.summary(),

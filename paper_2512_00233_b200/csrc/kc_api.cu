@@ -10,6 +10,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -22,6 +23,29 @@ using namespace kcb;
 namespace {
 
 thread_local std::string g_last_error;
+
+}  // namespace
+
+namespace kcb {
+cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t s) {
+  static std::once_flag once[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::call_once(once[dev & 63], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
+  return cudaMallocAsync(p, bytes ? bytes : 1, s);
+}
+void dfree(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+}  // namespace kcb
+
+namespace {
 
 kc_status fail(kc_status s, const std::string& msg) {
   g_last_error = msg;
@@ -135,20 +159,20 @@ namespace {
 
 void free_solver(kc_graph* g) {
   if (!g->solver_ready) return;
-  cudaFree(g->sb.est[0]);
-  cudaFree(g->sb.est[1]);
-  cudaFree(g->sb.cnt);
-  cudaFree(g->sb.queue);
-  cudaFree(g->sb.flag[0]);
-  cudaFree(g->sb.flag[1]);
-  cudaFree(g->sb.ctl);
-  cudaFree(g->sb.anydrop);
-  cudaFree(g->sb.stats);
-  cudaFree(g->sb.status);
-  cudaFree(g->d_out);
-  cudaFree(g->d_k);
-  cudaFree(g->d_prof);
-  cudaFree(g->d_count);
+  dfree(g->sb.est[0], g->stream);
+  dfree(g->sb.est[1], g->stream);
+  dfree(g->sb.cnt, g->stream);
+  dfree(g->sb.queue, g->stream);
+  dfree(g->sb.flag[0], g->stream);
+  dfree(g->sb.flag[1], g->stream);
+  dfree(g->sb.ctl, g->stream);
+  dfree(g->sb.anydrop, g->stream);
+  dfree(g->sb.stats, g->stream);
+  dfree(g->sb.status, g->stream);
+  dfree(g->d_out, g->stream);
+  dfree(g->d_k, g->stream);
+  dfree(g->d_prof, g->stream);
+  dfree(g->d_count, g->stream);
   g->d_prof = nullptr;
   g->d_count = nullptr;
   std::memset(&g->sb, 0, sizeof(g->sb));
@@ -168,23 +192,23 @@ kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
   b.n_nz = n_nz;
   for (int c = 0; c <= NCLS; ++c) b.cls_begin[c] = g->lay.cls_begin[c];
   g->solver_ready = true;  // so that partial allocations get freed
-  CK(cudaMalloc(&b.est[0], n_pad * es));
-  CK(cudaMalloc(&b.est[1], n_pad * es));
-  CK(cudaMalloc(&b.cnt, n_pad * sizeof(uint32_t)));
-  CK(cudaMalloc(&b.queue, n_pad * sizeof(uint32_t)));
-  CK(cudaMalloc(&b.flag[0], n_pad));
-  CK(cudaMalloc(&b.flag[1], n_pad));
+  CK(dmalloc((void**)&b.est[0], n_pad * es, g->stream));
+  CK(dmalloc((void**)&b.est[1], n_pad * es, g->stream));
+  CK(dmalloc((void**)&b.cnt, n_pad * sizeof(uint32_t), g->stream));
+  CK(dmalloc((void**)&b.queue, n_pad * sizeof(uint32_t), g->stream));
+  CK(dmalloc((void**)&b.flag[0], n_pad, g->stream));
+  CK(dmalloc((void**)&b.flag[1], n_pad, g->stream));
   CK(cudaMemsetAsync(b.est[0], 0, n_pad * es, g->stream));
   CK(cudaMemsetAsync(b.est[1], 0, n_pad * es, g->stream));
   CK(cudaMemsetAsync(b.flag[0], 0, n_pad, g->stream));
   CK(cudaMemsetAsync(b.flag[1], 0, n_pad, g->stream));
-  CK(cudaMalloc(&b.ctl, 2 * sizeof(Ctl)));
-  CK(cudaMalloc(&b.anydrop, 4 * sizeof(uint32_t)));
-  CK(cudaMalloc(&b.stats, (size_t)STAT_SLOTS * sizeof(RoundStat)));
-  CK(cudaMalloc(&b.status, 4 * sizeof(uint32_t)));
-  CK(cudaMalloc(&g->d_out, (g->n ? g->n : 1) * sizeof(uint32_t)));
-  CK(cudaMalloc(&g->d_k, 2 * sizeof(unsigned long long)));
-  CK(cudaMalloc(&g->d_count, sizeof(unsigned long long)));
+  CK(dmalloc((void**)&b.ctl, 2 * sizeof(Ctl), g->stream));
+  CK(dmalloc((void**)&b.anydrop, 4 * sizeof(uint32_t), g->stream));
+  CK(dmalloc((void**)&b.stats, (size_t)STAT_SLOTS * sizeof(RoundStat), g->stream));
+  CK(dmalloc((void**)&b.status, 4 * sizeof(uint32_t), g->stream));
+  CK(dmalloc((void**)&g->d_out, (g->n ? g->n : 1) * sizeof(uint32_t), g->stream));
+  CK(dmalloc((void**)&g->d_k, 2 * sizeof(unsigned long long), g->stream));
+  CK(dmalloc((void**)&g->d_count, sizeof(unsigned long long), g->stream));
   g->max_rounds = max_rounds;
   return KC_OK;
 }
@@ -224,7 +248,7 @@ uint32_t cache_entries(const kc_graph* g, const kc_options& o) {
 // estimates on the device.  Fills the counters of `st`.
 kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_t r_end) {
   if ((o.reserved[0] & KC_DEBUG_PHASE_TIMES) && !g->d_prof) {
-    CK(cudaMalloc(&g->d_prof, (size_t)PROF_ROUNDS * g->num_sms * PROF_PHASES * 8));
+    CK(dmalloc((void**)&g->d_prof, (size_t)PROF_ROUNDS * g->num_sms * PROF_PHASES * 8, g->stream));
     CK(cudaMemsetAsync(g->d_prof, 0, (size_t)PROF_ROUNDS * g->num_sms * PROF_PHASES * 8, g->stream));
   }
   g->sb.prof = (o.reserved[0] & KC_DEBUG_PHASE_TIMES) ? g->d_prof : nullptr;
@@ -329,11 +353,11 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
     if (csr->offsets[0] != 0 || csr->offsets[csr->n] != csr->nnz)
       return bail(fail(KC_ERR_INVALID_ARGUMENT, "offsets[0] != 0 or offsets[n] != nnz"));
     cudaEventRecord(g->ev[0], g->stream);
-    if ((e = cudaMalloc(&d_off, ((size_t)g->n + 1) * sizeof(uint64_t))) != cudaSuccess)
-      return bail(cuda_fail(e, "cudaMalloc offsets"));
-    if ((e = cudaMalloc(&d_adj, (g->nnz ? g->nnz : 1) * sizeof(uint32_t))) != cudaSuccess) {
-      cudaFree(d_off);
-      return bail(cuda_fail(e, "cudaMalloc neighbors"));
+    if ((e = dmalloc_n(&d_off, (size_t)g->n + 1, g->stream)) != cudaSuccess)
+      return bail(cuda_fail(e, "cudaMallocAsync offsets"));
+    if ((e = dmalloc_n(&d_adj, g->nnz, g->stream)) != cudaSuccess) {
+      dfree(d_off, g->stream);
+      return bail(cuda_fail(e, "cudaMallocAsync neighbors"));
     }
     e = cudaMemcpyAsync(d_off, csr->offsets, ((size_t)g->n + 1) * sizeof(uint64_t),
                         cudaMemcpyHostToDevice, g->stream);
@@ -341,8 +365,8 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
       e = cudaMemcpyAsync(d_adj, csr->neighbors, g->nnz * sizeof(uint32_t),
                           cudaMemcpyHostToDevice, g->stream);
     if (e != cudaSuccess) {
-      cudaFree(d_off);
-      cudaFree(d_adj);
+      dfree(d_off, g->stream);
+      dfree(d_adj, g->stream);
       return bail(cuda_fail(e, "cudaMemcpy H2D"));
     }
     cudaEventRecord(g->ev[1], g->stream);
@@ -357,8 +381,8 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
   cudaEventRecord(g->ev[2], g->stream);
   cudaStreamSynchronize(g->stream);
   if (!on_device) {
-    cudaFree(d_off);
-    cudaFree(d_adj);
+    dfree(d_off, g->stream);
+    dfree(d_adj, g->stream);
   }
   if (e != cudaSuccess) return bail(cuda_fail(e, "layout"));
   cudaEventElapsedTime(&g->t_upload, g->ev[0], g->ev[1]);
@@ -423,9 +447,10 @@ void kc_graph_free(kc_graph* g) {
   if (!g) return;
   cudaSetDevice(g->device);
   free_solver(g);
-  cudaFree(g->lay.off);
-  cudaFree(g->lay.adj);
-  cudaFree(g->lay.perm);
+  dfree(g->lay.off, g->stream);
+  dfree(g->lay.adj, g->stream);
+  dfree(g->lay.perm, g->stream);
+  if (g->stream) cudaStreamSynchronize(g->stream);
   for (auto& ev : g->ev)
     if (ev) cudaEventDestroy(ev);
   if (g->stream) cudaStreamDestroy(g->stream);

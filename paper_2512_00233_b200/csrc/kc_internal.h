@@ -87,6 +87,16 @@ cudaError_t launch_init(const SolveBuffers& b, bool est16, bool off64, uint32_t 
 // Max shared memory the solver may use for the estimate cache (bytes).
 size_t solver_cache_bytes_max();
 
+// Stream-ordered device allocation from the device's default memory pool,
+// kept (release threshold = max) so repeated upload / solve / free cycles do
+// not pay cudaMalloc / cudaFree (kc_api.cu).
+cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t s);
+void dfree(void* p, cudaStream_t s);
+template <typename T>
+inline cudaError_t dmalloc_n(T** p, size_t count, cudaStream_t s) {
+  return dmalloc(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T), s);
+}
+
 // On-device layout of an uploaded CSR (kc_prep.cu).
 struct PrepOut {
   void* off;        // OffT [n_nz + 1]

@@ -115,8 +115,8 @@ __global__ void chunk_count_kernel(const OffT* __restrict__ new_off, uint32_t n_
   } while (0)
 
 template <typename T>
-static cudaError_t dalloc(T** p, size_t count) {
-  return cudaMalloc(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T));
+static cudaError_t dalloc(T** p, size_t count, cudaStream_t s) {
+  return dmalloc_n(p, count, s);
 }
 
 // Relabel + narrow + sort rows.  `off`/`adj` are device pointers to the
@@ -140,18 +140,18 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
   out->adj = nullptr;
   out->perm = nullptr;
 
-  PREP_CK(dalloc(&deg, n));
-  PREP_CK(dalloc(&iota, n));
-  PREP_CK(dalloc(&sdeg, n));
-  PREP_CK(dalloc(&perm, n));
-  PREP_CK(dalloc(&inv, n));
-  PREP_CK(dalloc(&bounds, 8));
+  PREP_CK(dalloc(&deg, n, s));
+  PREP_CK(dalloc(&iota, n, s));
+  PREP_CK(dalloc(&sdeg, n, s));
+  PREP_CK(dalloc(&perm, n, s));
+  PREP_CK(dalloc(&inv, n, s));
+  PREP_CK(dalloc(&bounds, 8, s));
   degrees_kernel<<<G, B, 0, s>>>(off, n, deg, iota);
   PREP_CK(cudaGetLastError());
   // stable descending radix sort of (degree, id)
   PREP_CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, need, deg, sdeg, iota, perm, n, 0, 32, s));
   tmp_bytes = need;
-  PREP_CK(cudaMalloc(&tmp, tmp_bytes ? tmp_bytes : 1));
+  PREP_CK(dmalloc(&tmp, tmp_bytes, s));
   PREP_CK(cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, deg, sdeg, iota, perm, n, 0, 32, s));
   inverse_kernel<<<G, B, 0, s>>>(perm, n, inv);
   PREP_CK(cudaGetLastError());
@@ -169,7 +169,7 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
   {
     const uint32_t n_nz = out->n_nz;
     // new offsets: exclusive scan of sorted degrees (n_nz + 1 entries)
-    PREP_CK(dalloc(&off64_tmp, (size_t)n_nz + 1));
+    PREP_CK(dalloc(&off64_tmp, (size_t)n_nz + 1, s));
     PREP_CK(cudaMemsetAsync(off64_tmp, 0, sizeof(uint64_t), s));
     {
       auto in = cub::TransformInputIterator<uint64_t, cub::CastOp<uint64_t>, const uint32_t*>(
@@ -177,10 +177,10 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
       size_t nb = 0;
       PREP_CK(cub::DeviceScan::InclusiveSum(nullptr, nb, in, off64_tmp + 1, n_nz, s));
       if (nb > tmp_bytes) {
-        PREP_CK(cudaFree(tmp));
+        dfree(tmp, s);
         tmp = nullptr;
         tmp_bytes = nb;
-        PREP_CK(cudaMalloc(&tmp, tmp_bytes));
+        PREP_CK(dmalloc(&tmp, tmp_bytes, s));
       }
       PREP_CK(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, in, off64_tmp + 1, n_nz, s));
     }
@@ -188,13 +188,13 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
       new_off = off64_tmp;
       off64_tmp = nullptr;
     } else {
-      PREP_CK(cudaMalloc(&new_off, ((size_t)n_nz + 1) * sizeof(uint32_t)));
+      PREP_CK(dmalloc(&new_off, ((size_t)n_nz + 1) * sizeof(uint32_t), s));
       narrow_offsets_kernel<uint32_t><<<G, B, 0, s>>>(off64_tmp, n_nz + 1, (uint32_t*)new_off);
       PREP_CK(cudaGetLastError());
     }
-    PREP_CK(dalloc(&new_adj, nnz + ADJ_PAD));
+    PREP_CK(dalloc(&new_adj, nnz + ADJ_PAD, s));
     PREP_CK(cudaMemsetAsync(new_adj + nnz, 0, ADJ_PAD * sizeof(uint32_t), s));
-    PREP_CK(dalloc(&chunks, (size_t)n_nz + 1));
+    PREP_CK(dalloc(&chunks, (size_t)n_nz + 1, s));
     if (n_nz) {
       if (off64)
         chunk_count_kernel<uint64_t><<<G, B, 0, s>>>((const uint64_t*)new_off, n_nz, chunks);
@@ -204,10 +204,10 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
       size_t nb = 0;
       PREP_CK(cub::DeviceScan::ExclusiveSum(nullptr, nb, chunks, chunks, n_nz + 1, s));
       if (nb > tmp_bytes) {
-        PREP_CK(cudaFree(tmp));
+        dfree(tmp, s);
         tmp = nullptr;
         tmp_bytes = nb;
-        PREP_CK(cudaMalloc(&tmp, tmp_bytes));
+        PREP_CK(dmalloc(&tmp, tmp_bytes, s));
       }
       // chunks[n_nz] must be 0 before the exclusive scan so the total lands there
       PREP_CK(cudaMemsetAsync(chunks + n_nz, 0, sizeof(uint64_t), s));
@@ -224,7 +224,7 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
       PREP_CK(cudaGetLastError());
       // sort each row ascending (segmented sort over the new offsets)
       if (nnz > 0 && nnz < (1ull << 31)) {
-        PREP_CK(dalloc(&sort_tmp, nnz + ADJ_PAD));
+        PREP_CK(dalloc(&sort_tmp, nnz + ADJ_PAD, s));
         PREP_CK(cudaMemsetAsync(sort_tmp + nnz, 0, ADJ_PAD * sizeof(uint32_t), s));
         size_t nb2 = 0;
         if (off64) {
@@ -237,10 +237,10 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
                                                      (int64_t)n_nz, o, o + 1, s));
         }
         if (nb2 > tmp_bytes) {
-          PREP_CK(cudaFree(tmp));
+          dfree(tmp, s);
           tmp = nullptr;
           tmp_bytes = nb2;
-          PREP_CK(cudaMalloc(&tmp, tmp_bytes));
+          PREP_CK(dmalloc(&tmp, tmp_bytes, s));
         }
         if (off64) {
           const uint64_t* o = (const uint64_t*)new_off;
@@ -263,18 +263,18 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
   new_adj = nullptr;
   perm = nullptr;
 done:
-  cudaFree(deg);
-  cudaFree(iota);
-  cudaFree(sdeg);
-  cudaFree(perm);
-  cudaFree(inv);
-  cudaFree(bounds);
-  cudaFree(off64_tmp);
-  cudaFree(chunks);
-  cudaFree(new_off);
-  cudaFree(new_adj);
-  cudaFree(sort_tmp);
-  cudaFree(tmp);
+  dfree(deg, s);
+  dfree(iota, s);
+  dfree(sdeg, s);
+  dfree(perm, s);
+  dfree(inv, s);
+  dfree(bounds, s);
+  dfree(off64_tmp, s);
+  dfree(chunks, s);
+  dfree(new_off, s);
+  dfree(new_adj, s);
+  dfree(sort_tmp, s);
+  dfree(tmp, s);
   return err;
 }
 
