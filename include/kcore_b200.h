@@ -69,6 +69,7 @@ typedef struct kc_options {
 } kc_options;
 
 #define KC_DEBUG_PHASE_TIMES 1u /* record per-CTA per-round phase timestamps */
+#define KC_DEBUG_LEGACY_COUNT 2u /* counting rule on the flag-frontier solver (A/B) */
 
 /* RunReport (report.hpp:17-23) + work counters and timings. */
 typedef struct kc_stats {
@@ -155,6 +156,12 @@ void* kc_graph_stream(kc_graph* g);
  * [256 rounds][grid][8].  *grid receives the CTA count. */
 kc_status kc_debug_phase_times(kc_graph* g, unsigned long long* out, uint64_t cap,
                                uint32_t* grid);
+
+/* Debug: per-round counters of the last solve, 9 x uint64 per round
+ * (evaluations, sum of their degrees, drops, notifications, entries streamed
+ * by notify, entries streamed by evaluate, queue sizes HUGE|BIG<<32,
+ * WARP|SUB<<32, THREAD) for the first `rounds` rounds (at most 4096). */
+kc_status kc_debug_round_stats(kc_graph* g, unsigned long long* out, uint32_t rounds);
 
 /* ---- synthetic inputs (BASELINE.json configs; the "kcgen v1" spec) ------ */
 /* Build one of the five configs (1..5) — or a scaled variant — directly on

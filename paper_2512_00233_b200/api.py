@@ -63,8 +63,10 @@ ABI_SYMBOLS = (
     "kc_graph_nnz", "kc_graph_timings", "kc_solve", "kc_solve_device",
     "kc_solve_observed", "kc_fastk_run", "kc_graph_stream", "kc_gen_config",
     "kc_csr_dev_free", "kc_csr_dev_download", "kc_debug_phase_times", "kc_graph_upload_ex",
+    "kc_debug_round_stats",
 )
 KC_DEBUG_PHASE_TIMES = 1
+KC_DEBUG_LEGACY_COUNT = 2
 KC_UPLOAD_FORCE_OFF64 = 1
 KC_UPLOAD_FORCE_EST32 = 2
 
@@ -123,6 +125,8 @@ def load_library():
     L.kc_debug_phase_times.restype = C.c_int
     L.kc_debug_phase_times.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64,
                                        C.POINTER(C.c_uint32)]
+    L.kc_debug_round_stats.restype = C.c_int
+    L.kc_debug_round_stats.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32]
     L.kc_csr_dev_download.restype = C.c_int
     L.kc_csr_dev_download.argtypes = [C.POINTER(_CSRDev), C.c_void_p, C.c_void_p]
     _lib = L
@@ -418,6 +422,15 @@ class GpuGraph:
         _check(load_library().kc_debug_phase_times(self._h, buf.ctypes.data, buf.size,
                                                    C.byref(grid)), "kc_debug_phase_times")
         return buf[: 256 * grid.value * 8].reshape(256, grid.value, 8)
+
+    def round_stats(self, rounds: int) -> np.ndarray:
+        """[rounds, 9] per-round counters of the last solve (debug): evals,
+        escan (sum of degrees), drops, fires, nscan, ascan (entries streamed by
+        evaluate), HUGE|BIG<<32, WARP|SUB<<32, THREAD."""
+        buf = np.zeros((rounds, 9), dtype=np.uint64)
+        _check(load_library().kc_debug_round_stats(self._h, buf.ctypes.data, rounds),
+               "kc_debug_round_stats")
+        return buf
 
     def free(self) -> None:
         if getattr(self, "_h", None):

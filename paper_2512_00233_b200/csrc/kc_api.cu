@@ -163,6 +163,12 @@ void free_solver(kc_graph* g) {
   dfree(g->sb.est[1], g->stream);
   dfree(g->sb.cnt, g->stream);
   dfree(g->sb.queue, g->stream);
+  dfree(g->sb.queue2, g->stream);
+  dfree(g->sb.radj, g->stream);
+  dfree(g->sb.rlen, g->stream);
+  dfree(g->sb.rthr, g->stream);
+  dfree(g->sb.lq[0], g->stream);
+  dfree(g->sb.lq[1], g->stream);
   dfree(g->sb.flag[0], g->stream);
   dfree(g->sb.flag[1], g->stream);
   dfree(g->sb.ctl, g->stream);
@@ -196,6 +202,15 @@ kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
   CK(dmalloc((void**)&b.est[1], n_pad * es, g->stream));
   CK(dmalloc((void**)&b.cnt, n_pad * sizeof(uint32_t), g->stream));
   CK(dmalloc((void**)&b.queue, n_pad * sizeof(uint32_t), g->stream));
+  CK(dmalloc((void**)&b.queue2, n_pad * sizeof(uint32_t), g->stream));
+  CK(dmalloc((void**)&b.rlen, n_pad * sizeof(uint32_t), g->stream));
+  CK(dmalloc((void**)&b.rthr, n_pad * es, g->stream));
+  CK(dmalloc((void**)&b.radj, ((size_t)g->nnz + ADJ_PAD) * sizeof(uint32_t), g->stream));
+  CK(cudaMemsetAsync(b.radj + g->nnz, 0, ADJ_PAD * sizeof(uint32_t), g->stream));
+  for (int ph = 0; ph < 2; ++ph) {  // slots hold 0xffffffff while empty
+    CK(dmalloc((void**)&b.lq[ph], ((size_t)b.cls_begin[1] + 1) * sizeof(uint32_t), g->stream));
+    CK(cudaMemsetAsync(b.lq[ph], 0xff, ((size_t)b.cls_begin[1] + 1) * sizeof(uint32_t), g->stream));
+  }
   CK(dmalloc((void**)&b.flag[0], n_pad, g->stream));
   CK(dmalloc((void**)&b.flag[1], n_pad, g->stream));
   CK(cudaMemsetAsync(b.est[0], 0, n_pad * es, g->stream));
@@ -232,6 +247,12 @@ kc_status validate(const kc_options* opt, kc_options* o) {
   return KC_OK;
 }
 
+// The counting rule runs on kc_count.cu's solver (lists + direct queues)
+// unless the legacy flag-frontier solver is requested for A/B runs.
+bool uses_count_kernel(const kc_options& o) {
+  return map_rule(o) == R_COUNT && !(o.reserved[0] & KC_DEBUG_LEGACY_COUNT);
+}
+
 uint32_t cache_entries(const kc_graph* g, const kc_options& o) {
   if (o.smem_cache == 0xffffffffu) return 0;
   const size_t es = g->est16 ? 2 : 4;
@@ -259,7 +280,18 @@ kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_
   c.max_rounds = o.max_rounds;
   c.tail_threshold = 0;
   c.num_sms = g->num_sms;
-  CK(launch_rounds(g->sb, c, g->est16, g->lay.off64, r_begin, r_end, g->stream));
+  if (uses_count_kernel(o))
+    CK(launch_count_rounds(g->sb, c, g->est16, g->lay.off64, r_begin, r_end, g->stream));
+  else
+    CK(launch_rounds(g->sb, c, g->est16, g->lay.off64, r_begin, r_end, g->stream));
+  return KC_OK;
+}
+
+kc_status init_state(kc_graph* g, const kc_options& o) {
+  if (uses_count_kernel(o))
+    CK(launch_count_init(g->sb, g->est16, g->lay.off64, g->lay.h_graph, g->stream));
+  else
+    CK(launch_init(g->sb, g->est16, g->lay.off64, g->lay.h_graph, o.max_rounds, g->stream));
   return KC_OK;
 }
 
@@ -499,7 +531,8 @@ static kc_status solve_impl(kc_graph* g, const kc_options* opt, uint32_t* out, b
   s = ensure_solver(g, o.max_rounds);
   if (s != KC_OK) return s;
   CK(cudaEventRecord(g->ev[0], g->stream));
-  CK(launch_init(g->sb, g->est16, g->lay.off64, g->lay.h_graph, o.max_rounds, g->stream));
+  s = init_state(g, o);
+  if (s != KC_OK) return s;
   s = run_rounds(g, o, 0, o.max_rounds);
   if (s != KC_OK) return s;
   CK(cudaEventRecord(g->ev[1], g->stream));
@@ -560,7 +593,8 @@ kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn 
   }
   s = ensure_solver(g, o.max_rounds);
   if (s != KC_OK) return s;
-  CK(launch_init(g->sb, g->est16, g->lay.off64, g->lay.h_graph, o.max_rounds, g->stream));
+  s = init_state(g, o);
+  if (s != KC_OK) return s;
   // iteration 0: the reference reports est = degree (fastk.cpp:67-68, 93)
   if (g->lay.off64)
     degree_back_kernel<uint64_t><<<g->num_sms * 4, 256, 0, g->stream>>>(
@@ -579,7 +613,13 @@ kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn 
     s = collect(g, o, nullptr, &conv);
     if (s != KC_OK) return s;
     unsigned long long active = 0;
-    if (!conv) {  // flags collected for round r+1 (the reference's active_count)
+    if (!conv && uses_count_kernel(o)) {  // round r+1's queue sizes
+      Ctl ctl;
+      CK(cudaMemcpyAsync(&ctl, g->sb.ctl + ((r + 1) & 1), sizeof(Ctl), cudaMemcpyDeviceToHost,
+                         g->stream));
+      CK(cudaStreamSynchronize(g->stream));
+      for (int c = 0; c < NCLS; ++c) active += ctl.qcnt[c];
+    } else if (!conv) {  // flags collected for round r+1 (the reference's active_count)
       CK(cudaMemsetAsync(g->d_count, 0, sizeof(unsigned long long), g->stream));
       count_flags_kernel<<<g->num_sms * 2, 256, 0, g->stream>>>(g->sb.flag[(r + 1) & 1],
                                                                 g->lay.n_nz, g->d_count);
@@ -609,6 +649,14 @@ kc_status kc_debug_phase_times(kc_graph* g, unsigned long long* out, uint64_t ca
   if (!g->d_prof) return fail(KC_ERR_INVALID_ARGUMENT, "no phase times recorded");
   const uint64_t total = (uint64_t)PROF_ROUNDS * g->num_sms * PROF_PHASES;
   CK(cudaMemcpy(out, g->d_prof, (cap < total ? cap : total) * 8, cudaMemcpyDeviceToHost));
+  return KC_OK;
+}
+
+kc_status kc_debug_round_stats(kc_graph* g, unsigned long long* out, uint32_t rounds) {
+  if (!g || !out) return fail(KC_ERR_INVALID_ARGUMENT, "null argument");
+  if (!g->sb.stats) return fail(KC_ERR_INVALID_ARGUMENT, "no solve has run");
+  const uint32_t k = rounds < STAT_SLOTS ? rounds : STAT_SLOTS;
+  CK(cudaMemcpy(out, g->sb.stats, (size_t)k * sizeof(RoundStat), cudaMemcpyDeviceToHost));
   return KC_OK;
 }
 

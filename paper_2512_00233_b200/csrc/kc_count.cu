@@ -1,0 +1,1095 @@
+// kc_count.cu — the counting-rule FastK solver (KC_RULE_COUNTING, the
+// default): one persistent cooperative kernel on sm_100a.
+//
+// Reference path (paths under /root/reference/proj):
+//   fastk_run            src/fastk.cpp:57-187  — rounds of process | apply | notify
+//   compute_index_over   include/kcore/kernel.hpp:27-42 — capped h-index
+//   should_notify        include/kcore/fastk.hpp:25-27  — extended activation rule
+//
+// Same Jacobi trajectory as the reference (and as kc_solve.cu), organised
+// around three facts of the counting rule:
+//
+//  1. Support counters.  cnt[v] = #{w in N(v) : est_w >= est_v}.  A drop
+//     u: cap -> t passes should_notify(t, cap, N[w]) exactly when it removes
+//     u from w's count; the one decrement that takes cnt[w] below N[w] makes
+//     w unstable.  So a vertex is evaluated iff it drops, and the decrement
+//     that activates it is unique: it is appended to the next round's queue
+//     directly (per-warp shared-memory buffers, one global atomic per 32
+//     activations) — no frontier flags, no compaction pass.
+//
+//  2. The answer is bracketed.  An active u has lo = cnt[u] = count(>= cap)
+//     < cap, and its new level t satisfies lo <= t < cap.  Only neighbour
+//     values in [lo, cap) are binned.
+//
+//  3. Relevant-neighbour lists.  After its first drop, u keeps in `radj` the
+//     neighbours w with est_w >= L_u (L_u = ceil(t/2) at build time).
+//     Estimates only fall, so every neighbour left out stays below L_u
+//     forever.  While t >= L_u, both the h-index (levels >= L_u) and the
+//     notify test (N[w] > t) are decided by the list alone; a hub with 160 K
+//     neighbours and t ~ 900 scans a few thousand entries per round instead
+//     of its whole row.  If the answer falls below L_u (lo < L_u and t < L_u)
+//     the evaluation scans the CSR row, and the notify pass that follows
+//     rebuilds the list.  E_scan is still reported as the sum of degrees
+//     (the algorithmic convention of SURVEY §8(d)).
+//
+// Round r:
+//   EVALUATE  every queued u (round 0: every vertex) computes t and
+//             c = count(E >= t); writes N[u] = t, cnt[u] = c.
+//   --- grid.sync (round 0 without a drop ends here, fastk.cpp:109-110) ---
+//   NOTIFY    every dropper streams its list (or row) against the settled
+//             values N, decrements cnt[w] where should_notify holds,
+//             enqueues the w whose counter crossed below N[w], applies
+//             E[u] = t (fastk.cpp:153).
+//   --- grid.sync ---
+// An empty queue at a round start is the quiescent round: converged.
+#include <cooperative_groups.h>
+#include <cstdint>
+
+#include "kc_dev.cuh"
+#include "kc_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace kcb {
+namespace {
+using namespace dev;
+
+constexpr uint32_t GMAX_BIG = 2, GMAX_WARP = 8, GMAX_SMALL = 32;  // items per grab (max)
+constexpr uint32_t CACHE_MIN_ACTIVE = 4096;  // smaller rounds skip the shared-memory cache
+#ifndef KC_LIST_MIN_DEG
+#define KC_LIST_MIN_DEG 64
+#endif
+constexpr uint32_t LIST_MIN_DEG = KC_LIST_MIN_DEG;  // rows longer than this keep a list
+constexpr uint32_t WARP_MAX_LEN = DEG_BIG_MAX;  // longest scan a single warp takes
+constexpr int WQ = 64;             // per-warp, per-class enqueue buffer (flushed at 32)
+#ifndef KC_LIST_COMPACT
+#define KC_LIST_COMPACT 0          // 1: notify filters lists in place (warp scans)
+#endif
+#ifndef KC_LIST_SHIFT
+#define KC_LIST_SHIFT 1            // list threshold L = t - (t >> KC_LIST_SHIFT)
+#endif
+
+template <typename OffT, typename EstT>
+struct CP {
+  const OffT* off;
+  const uint32_t* adj;  // CSR rows (immutable)
+  uint32_t* radj;       // relevant-neighbour lists, row u at off[u]
+  uint32_t* rlen;       // list lengths
+  EstT* rthr;           // list thresholds L_u (0: no list, use the CSR row)
+  uint32_t n_nz;
+  uint32_t cb[NCLS + 1];
+  EstT* E;  // snapshot
+  EstT* N;  // settled
+  uint32_t* cnt;
+  uint32_t* queue[2];  // queue[r & 1]: round r's active ids, class c at offset cb[c]
+  uint32_t* lq[2];     // long-scan queues (evaluate, notify); empty slots 0xffffffff
+  Ctl* ctl;            // [2] per round parity: qcnt (queue sizes), grab / grab2 cursors
+  uint32_t* anydrop;   // [0]: some estimate dropped in round 0
+  RoundStat* stats;
+  uint32_t* status;
+  unsigned long long* prof;
+  uint32_t r_begin, r_end, cache_n, clamp_drop;
+};
+
+template <typename EstT>
+struct View {
+  const EstT* snap;      // gathered estimates: E (evaluate) or N (notify)
+  const uint32_t* q;     // this round's queue; nullptr in round 0 (ids implicit)
+  const uint32_t* qcnt;  // this round's class sizes
+  uint32_t* grab;        // cursors of the current phase
+  uint32_t* qn;          // next round's class sizes
+  uint32_t* qnext;       // next round's queue
+  uint32_t cache_n;      // ids cached in shared memory this phase (0: none)
+  bool r0;
+};
+
+struct Acc {  // per-thread counters, flushed per round
+  unsigned long long evals, escan, drops, fires, nscan, ascan;
+  bool any_drop;
+};
+
+struct Shared {  // per-CTA bookkeeping (static shared memory)
+  uint32_t red[33];
+  uint32_t item;
+  uint32_t drop;
+  uint32_t ticket;            // long-scan queue ticket held across the phase
+  uint32_t cursor;            // CTA list-build cursor
+  uint32_t out[2];
+  unsigned long long acc[6];
+};
+
+template <typename OffT, typename EstT>
+__device__ __forceinline__ int cls_of(const CP<OffT, EstT>& p, uint32_t id) {
+  return (int)(id >= p.cb[1]) + (int)(id >= p.cb[2]) + (int)(id >= p.cb[3]) +
+         (int)(id >= p.cb[4]);
+}
+
+// Grab size for class c this round: up to gmax items per atomic, fewer when
+// the queue is short so that every warp gets work.
+__device__ __forceinline__ uint32_t grab_size(uint32_t cnt, uint32_t gmax) {
+  const uint32_t per = cnt / (gridDim.x * NWARPS * 2u);
+  return per < 1u ? 1u : per > gmax ? gmax : per;
+}
+
+// Warp-level queue walk: `proc(u, n)` gets the warp's slice, lane i holding
+// item i (i < n).
+template <typename OffT, typename EstT, typename F>
+__device__ __forceinline__ void for_class(const CP<OffT, EstT>& p, const View<EstT>& v, int c,
+                                          uint32_t gmax, F&& proc) {
+  const uint32_t cnt = v.qcnt[c];
+  if (cnt == 0) return;
+  const uint32_t G = grab_size(cnt, gmax);
+  uint32_t* cursor = &v.grab[c];
+  const uint32_t lane = lane_id();
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0)  // plain read first: no atomic once the queue is drained
+      base = *reinterpret_cast<volatile uint32_t*>(cursor) >= cnt ? cnt : atomicAdd(cursor, G);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= cnt) break;
+    const uint32_t n = cnt - base < G ? cnt - base : G;
+    uint32_t u = 0;
+    if (lane < n) u = v.q ? v.q[p.cb[c] + base + lane] : p.cb[c] + base + lane;
+    proc(u, n);
+  }
+}
+
+// ------------------------------------------------------------------------
+// Enqueue (notify phase, warp-converged): lanes' activations `act` (bit k:
+// ids[k]) go to the warp's shared buffer of their class; a buffer holding
+// >= 32 ids is flushed with one global atomicAdd.
+// ------------------------------------------------------------------------
+template <typename OffT, typename EstT>
+__device__ __noinline__ void wq_flush(const CP<OffT, EstT>& p, const View<EstT>& v, uint32_t* wbuf,
+                                      uint32_t* wn, int c) {
+  const uint32_t n = wn[c];
+  if (n == 0) return;
+  uint32_t base = 0;
+  if (lane_id() == 0) base = atomicAdd(&v.qn[c], n);
+  base = __shfl_sync(FULL, base, 0);
+  for (uint32_t i = lane_id(); i < n; i += 32) v.qnext[p.cb[c] + base + i] = wbuf[c * WQ + i];
+  __syncwarp();
+  if (lane_id() == 0) wn[c] = 0;
+  __syncwarp();
+}
+
+template <typename OffT, typename EstT>
+__device__ __noinline__ void wq_push(const CP<OffT, EstT>& p, const View<EstT>& v, uint32_t* wbuf,
+                                     uint32_t* wn, uint32_t act, const uint32_t (&ids)[8]) {
+#pragma unroll 1
+  for (int k = 0; k < 8; ++k) {
+    const bool a = act >> k & 1;
+    if (!__any_sync(FULL, a)) continue;
+    uint32_t id = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j == k) id = ids[j];
+    const int c = a ? cls_of(p, id) : NCLS;
+#pragma unroll 1
+    for (int cc = 0; cc < NCLS; ++cc) {
+      const uint32_t m = __ballot_sync(FULL, c == cc);
+      if (!m) continue;
+      const uint32_t n0 = wn[cc];
+      if (c == cc) wbuf[cc * WQ + n0 + __popc(m & lanemask_lt())] = id;
+      __syncwarp();
+      if (lane_id() == 0) wn[cc] = n0 + __popc(m);
+      __syncwarp();
+      if (n0 + __popc(m) >= 32) wq_flush(p, v, wbuf, wn, cc);
+    }
+  }
+}
+
+// What a dropper u (cap -> t) does to 8 neighbours ids[k] with settled levels
+// x[k] (valid where bit k of ok): decrement cnt[w] where should_notify(t,
+// cap, N[w]) holds (fastk.hpp:25-27); the decrement that takes cnt[w] below
+// N[w] activates w.  All atomics are issued before any result is consumed.
+template <typename OffT, typename EstT>
+__device__ __forceinline__ void notify8(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                        uint32_t* wbuf, uint32_t* wn, uint32_t ok,
+                                        const uint32_t (&ids)[8], const uint32_t (&x)[8],
+                                        uint32_t t, uint32_t cap, Acc& acc) {
+  uint32_t fire = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) fire |= (uint32_t)((ok >> k & 1) && t < x[k] && x[k] <= cap) << k;
+  uint32_t act = 0;
+  if (fire) {
+    acc.fires += __popc(fire);
+    uint32_t old[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) old[k] = (fire >> k & 1) ? atomicSub(&p.cnt[ids[k]], 1u) : 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) act |= (uint32_t)((fire >> k & 1) && old[k] == x[k]) << k;
+  }
+  if (__any_sync(FULL, act)) wq_push(p, v, wbuf, wn, act, ids);
+}
+
+// ------------------------------------------------------------------------
+// Windowed h-index over one row or list (kernel.hpp:31-41), values >= top
+// counted in registers, [top - NB, top) binned in shared memory, levels
+// below `lo` skipped (the answer is >= lo).  Returns (t, count(>= t)).
+// ------------------------------------------------------------------------
+template <bool RO, typename EstT>
+__device__ __noinline__ uint2 warp_window(const uint32_t* src, const EstT* snap,
+                                          const EstT* s_cache, uint32_t cache_n, uint32_t* bins,
+                                          uint64_t ob, uint64_t oe, uint32_t cap, uint32_t lo,
+                                          uint32_t deg) {
+  uint32_t top = cap;
+  for (;;) {
+    warp_zero_bins(bins);
+    uint32_t above = 0;
+    stream_row<32, RO>(src, snap, lane_id(), ob, oe, s_cache, cache_n,
+                       [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
+#pragma unroll
+                         for (int k = 0; k < 8; ++k)
+                           if (ok >> k & 1) tally<WARP_BINS>(x[k], top, lo, above, bins);
+                       });
+    __syncwarp();
+    const uint32_t C = __reduce_add_sync(FULL, above);
+    uint32_t level = 0, c = 0;
+    const bool hit = warp_resolve(bins, C, top, level, c, lo > 1u ? lo : 1u);
+    __syncwarp();
+    if (hit) return make_uint2(level, c);
+    if ((int)top - WARP_BINS <= (int)lo) return make_uint2(0u, deg);  // only level 0 left
+    top -= WARP_BINS;
+  }
+}
+
+template <bool RO, typename EstT>
+__device__ __noinline__ void cta_window(const uint32_t* src, const EstT* snap, const EstT* s_cache,
+                                        uint32_t cache_n, uint32_t* s_hist, uint32_t* s_red,
+                                        uint64_t ob, uint64_t oe, uint32_t cap, uint32_t lo,
+                                        uint32_t deg, uint32_t* out) {
+  const uint32_t tid = threadIdx.x;
+  uint32_t top = cap;
+  for (;;) {
+    for (int i = tid; i < HIST_BINS; i += SOLVE_THREADS) s_hist[i] = 0;
+    __syncthreads();
+    uint32_t above = 0;
+    stream_row<SOLVE_THREADS, RO>(src, snap, tid, ob, oe, s_cache, cache_n,
+                                  [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
+#pragma unroll
+                                    for (int k = 0; k < 8; ++k)
+                                      if (ok >> k & 1) tally<HIST_BINS>(x[k], top, lo, above, s_hist);
+                                  });
+    const uint32_t C = block_sum(above, s_red);
+    constexpr int PER = HIST_BINS / SOLVE_THREADS;
+    uint32_t h[PER];
+    uint32_t sm = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      h[j] = s_hist[tid * PER + j];
+      sm += h[j];
+    }
+    uint32_t run = C + block_excl_scan(sm, s_red);
+    const uint32_t minlvl = lo > 1u ? lo : 1u;  // levels below the floor are incomplete
+    uint32_t found = 0xffffffffu, frun = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      run += h[j];
+      const int i = tid * PER + j;
+      const int x = (int)top - 1 - i;
+      if (found == 0xffffffffu && x >= (int)minlvl && run >= (uint32_t)x) {
+        found = (uint32_t)i;
+        frun = run;
+      }
+    }
+    const uint32_t g = block_min(found, s_red);
+    if (g != 0xffffffffu) {
+      if (found == g) {
+        out[0] = top - 1 - g;
+        out[1] = frun;
+      }
+      __syncthreads();
+      return;
+    }
+    if ((int)top - HIST_BINS <= (int)lo) {
+      if (tid == 0) {
+        out[0] = 0;
+        out[1] = deg;
+      }
+      __syncthreads();
+      return;
+    }
+    top -= HIST_BINS;
+  }
+}
+
+// count(x >= cap) over a row (round 0's "no change" test), warp / CTA.
+template <typename EstT>
+__device__ __forceinline__ uint32_t warp_count_ge(const uint32_t* adj, const EstT* snap,
+                                                  const EstT* s_cache, uint32_t cache_n,
+                                                  uint64_t ob, uint64_t oe, uint32_t cap) {
+  uint32_t c = 0;
+  stream_row<32, true>(adj, snap, lane_id(), ob, oe, s_cache, cache_n,
+                       [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
+#pragma unroll
+                         for (int k = 0; k < 8; ++k) c += (ok >> k & 1) && x[k] >= cap;
+                       });
+  return __reduce_add_sync(FULL, c);
+}
+
+// ------------------------------------------------------------------------
+// One evaluation (vertex u, estimate cap, lower bound lo = cnt[u] in rounds
+// >= 1).  Round 0 first counts values >= cap ("no change" = one pass).
+// ------------------------------------------------------------------------
+struct Item {
+  uint32_t u, cap, lo, thr, len, deg;
+  uint64_t ob;
+  bool list;
+};
+
+// A vertex with a list (thr != 0) is first evaluated on it: levels >= thr
+// are decided by the list alone.  Only if no level >= max(lo, thr)
+// qualifies does the CSR row get scanned.
+template <typename OffT, typename EstT>
+__device__ __forceinline__ Item eval_item(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                          const EstT* s_cache, uint32_t u) {
+  Item it;
+  it.u = u;
+  it.ob = p.off[u];
+  it.deg = (uint32_t)(p.off[u + 1] - it.ob);
+  it.cap = est_at(s_cache, v.cache_n, v.snap, u);
+  it.lo = v.r0 ? 0u : p.cnt[u];
+  it.thr = (v.r0 || it.deg <= LIST_MIN_DEG) ? 0u : (uint32_t)p.rthr[u];
+  it.list = it.thr != 0;
+  it.len = it.list ? p.rlen[u] : it.deg;
+  return it;
+}
+
+template <typename OffT, typename EstT>
+__device__ __forceinline__ void finish_eval(const CP<OffT, EstT>& p, const Item& it, uint32_t t,
+                                            uint32_t c, uint32_t scanned, Acc& acc) {
+  acc.evals += 1;
+  acc.escan += it.deg;
+  acc.ascan += scanned;
+  p.cnt[it.u] = c;
+  if (t < it.cap) {
+    p.N[it.u] = (EstT)t;
+    acc.drops += 1;
+    acc.any_drop = true;
+  }
+  // the answer fell below the list threshold: the list is no longer
+  // sufficient for the notify test; the notify pass rebuilds it
+  if (it.thr != 0 && t < it.thr) p.rthr[it.u] = 0;
+}
+
+template <typename OffT, typename EstT>
+__device__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                          uint32_t* bins, const Item& it, Acc& acc) {
+  const EstT* snap = v.snap;
+  const uint32_t cache_n = v.cache_n;
+  uint32_t lo = it.lo;
+  if (v.r0) {
+    const uint32_t cA = warp_count_ge(p.adj, snap, s_cache, cache_n, it.ob, it.ob + it.deg, it.cap);
+    if (cA >= it.cap) {
+      if (lane_id() == 0) finish_eval(p, it, it.cap, cA, it.deg, acc);
+      return;
+    }
+    lo = cA;  // count(>= cA) >= count(>= cap) = cA: the answer is >= cA
+  }
+  uint2 tc = make_uint2(0, 0);
+  uint32_t scanned = 0;
+  if (it.list) {
+    tc = warp_window<false>(p.radj, snap, s_cache, cache_n, bins, it.ob, it.ob + it.len, it.cap,
+                            lo > it.thr ? lo : it.thr, it.deg);
+    scanned = it.len;
+  }
+  if (tc.x == 0) {  // no list, or the answer is below its threshold
+    tc = warp_window<true>(p.adj, snap, s_cache, cache_n, bins, it.ob, it.ob + it.deg, it.cap, lo,
+                           it.deg);
+    scanned += it.deg;
+  }
+  if (lane_id() == 0) finish_eval(p, it, tc.x, tc.y, scanned, acc);
+}
+
+template <typename OffT, typename EstT>
+__device__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                         uint32_t* s_hist, Shared& sh, uint32_t u, Acc& acc) {
+  const Item it = eval_item(p, v, s_cache, u);
+  const EstT* snap = v.snap;
+  const uint32_t cache_n = v.cache_n;
+  uint32_t lo = it.lo;
+  if (v.r0) {
+    uint32_t c = 0;
+    stream_row<SOLVE_THREADS, true>(p.adj, snap, threadIdx.x, it.ob, it.ob + it.deg, s_cache,
+                                    cache_n,
+                                    [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
+#pragma unroll
+                                      for (int k = 0; k < 8; ++k) c += (ok >> k & 1) && x[k] >= it.cap;
+                                    });
+    const uint32_t cA = block_sum(c, sh.red);
+    if (cA >= it.cap) {
+      if (threadIdx.x == 0) finish_eval(p, it, it.cap, cA, it.deg, acc);
+      __syncthreads();
+      return;
+    }
+    lo = cA;
+  }
+  uint32_t scanned = 0;
+  if (it.list) {
+    cta_window<false>(p.radj, snap, s_cache, cache_n, s_hist, sh.red, it.ob, it.ob + it.len,
+                      it.cap, lo > it.thr ? lo : it.thr, it.deg, sh.out);
+    scanned = it.len;
+  } else if (threadIdx.x == 0) {
+    sh.out[0] = 0;
+  }
+  __syncthreads();
+  if (sh.out[0] == 0) {
+    cta_window<true>(p.adj, snap, s_cache, cache_n, s_hist, sh.red, it.ob, it.ob + it.deg, it.cap,
+                     lo, it.deg, sh.out);
+    scanned += it.deg;
+  }
+  if (threadIdx.x == 0) finish_eval(p, it, sh.out[0], sh.out[1], scanned, acc);
+  __syncthreads();
+}
+
+// HUGE class.  Warps grab hubs one at a time and take those whose scan
+// (list or row) is at most WARP_MAX_LEN; longer ones are appended to the
+// phase's global long-scan queue, which CTAs drain one hub at a time
+// (CTA-wide scan).  consume_long(false) takes what is already queued;
+// consume_long(true) — at the end of the phase — keeps taking tickets until
+// every CTA has finished appending and no ticket is left.
+constexpr uint32_t NONE = 0xffffffffu;
+
+template <typename OffT, typename EstT, typename Long, typename WarpF>
+__device__ void huge_warps(const CP<OffT, EstT>& p, const View<EstT>& v, Shared& sh, Ctl& ctl,
+                           int ph, Long&& is_long, WarpF&& warp_fn) {
+  const uint32_t cnt = v.qcnt[C_HUGE];
+  if (cnt == 0) return;  // CTA- and grid-uniform
+  uint32_t* cursor = &v.grab[C_HUGE];
+  for (;;) {
+    uint32_t k = 0;
+    if (lane_id() == 0)
+      k = *reinterpret_cast<volatile uint32_t*>(cursor) >= cnt ? cnt : atomicAdd(cursor, 1u);
+    k = __shfl_sync(FULL, k, 0);
+    if (k >= cnt) break;
+    const uint32_t u = v.q ? v.q[p.cb[C_HUGE] + k] : p.cb[C_HUGE] + k;
+    if (is_long(u)) {
+      if (lane_id() == 0) {
+        const uint32_t slot = atomicAdd(&ctl.lqn[ph], 1u);
+        atomicExch(&p.lq[ph][slot], u);
+      }
+      continue;
+    }
+    warp_fn(u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&ctl.lqd[ph], 1u);
+  }
+}
+
+template <typename OffT, typename EstT, typename CtaF>
+__device__ void consume_long(const CP<OffT, EstT>& p, const View<EstT>& v, Shared& sh, Ctl& ctl,
+                             int ph, bool wait, CtaF&& cta_fn) {
+  if (v.qcnt[C_HUGE] == 0) return;
+  volatile uint32_t* lqn = &ctl.lqn[ph];
+  volatile uint32_t* lqc = &ctl.lqc[ph];
+  volatile uint32_t* lqd = &ctl.lqd[ph];
+  volatile uint32_t* lq = p.lq[ph];
+  for (;;) {
+    if (threadIdx.x == 0) {
+      uint32_t k = sh.ticket, u = NONE;
+      if (k == NONE && (wait || *lqc < *lqn)) k = atomicAdd(const_cast<uint32_t*>(lqc), 1u);
+      while (k != NONE) {
+        if (k < *lqn) {
+          while ((u = lq[k]) == NONE) {}  // the appender's store is in flight
+          lq[k] = NONE;
+          k = NONE;
+        } else if (!wait) {
+          break;  // keep the ticket for the final drain
+        } else if (*lqd == gridDim.x) {
+          __threadfence();
+          if (k >= *lqn) k = NONE;  // every hub is taken: done
+        } else {
+          __nanosleep(256);
+        }
+      }
+      sh.ticket = k;
+      sh.item = u;
+    }
+    __syncthreads();
+    const uint32_t u = sh.item;
+    __syncthreads();
+    if (u == NONE) break;
+    cta_fn(u);
+  }
+}
+
+// WARP and BIG classes: warp per vertex; metadata of a grab loaded one lane
+// per item, then walked.
+template <typename OffT, typename EstT>
+__device__ __noinline__ void eval_wclass(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                            uint32_t* bins, int c, uint32_t gmax, Acc& acc) {
+  for_class(p, v, c, gmax, [&](uint32_t u, uint32_t n) {
+    Item mine{};
+    if (lane_id() < n) mine = eval_item(p, v, s_cache, u);
+    for (uint32_t i = 0; i < n; ++i) {
+      Item it;
+      it.u = __shfl_sync(FULL, mine.u, i);
+      it.cap = __shfl_sync(FULL, mine.cap, i);
+      it.lo = __shfl_sync(FULL, mine.lo, i);
+      it.thr = __shfl_sync(FULL, mine.thr, i);
+      it.len = __shfl_sync(FULL, mine.len, i);
+      it.deg = __shfl_sync(FULL, mine.deg, i);
+      it.ob = __shfl_sync(FULL, mine.ob, i);
+      it.list = __shfl_sync(FULL, (uint32_t)mine.list, i) != 0;
+      eval_warp(p, v, s_cache, bins, it, acc);
+    }
+  });
+}
+
+// SUB class (deg <= 64): 8-lane tile per vertex, 8 values per lane,
+// bisection on [lo, cap).
+template <typename OffT, typename EstT>
+__device__ __noinline__ void eval_sub(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                         Acc& acc) {
+  constexpr int R = DEG_SUB_MAX / 8;
+  const uint32_t g = lane_id() >> 3, k = lane_id() & 7;
+  const EstT* snap = v.snap;
+  const uint32_t cache_n = v.cache_n;
+  const bool r0 = v.r0;
+  for_class(p, v, C_SUB, GMAX_SMALL, [&](uint32_t mu, uint32_t n) {
+    // metadata of the grab, one lane per item, loaded in parallel
+    uint64_t mob = 0;
+    uint32_t mdeg = 0, mcap = 0, mlo = 0;
+    if (lane_id() < n) {
+      mob = p.off[mu];
+      mdeg = (uint32_t)(p.off[mu + 1] - mob);
+      mcap = est_at(s_cache, cache_n, snap, mu);
+      mlo = r0 ? 0u : p.cnt[mu];
+    }
+    for (uint32_t i0 = 0; i0 < n; i0 += 4) {
+      // every lane runs the shuffles; tiles beyond n idle
+      const int src = (int)(i0 + g) & 31;
+      const uint32_t u = __shfl_sync(FULL, mu, src);
+      const bool has = i0 + g < n;
+      const uint64_t ob = __shfl_sync(FULL, mob, src);
+      const uint32_t sdeg = __shfl_sync(FULL, mdeg, src);  // shuffles by every lane
+      const uint32_t scap = __shfl_sync(FULL, mcap, src);
+      const uint32_t deg = has ? sdeg : 0u;
+      const uint32_t cap = has ? scap : 0u;
+      const uint32_t lo = __shfl_sync(FULL, mlo, src);
+      Vals<EstT, R> vals;
+      vals.clear();
+      {
+        uint32_t ids[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const uint32_t q = k + 8 * j;
+          ids[j] = q < deg ? p.adj[ob + q] : 0xffffffffu;
+        }
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          if (ids[j] != 0xffffffffu) vals.set(j, est_at(s_cache, cache_n, snap, ids[j]));
+      }
+      const uint32_t cA = tile8_sum(vals.count_ge(cap));
+      uint32_t lo_b = lo, hi = cap;  // invariant: count(>= lo_b) >= lo_b
+#pragma unroll 1
+      for (int s = 0; s < 7; ++s) {  // cap <= 64
+        const uint32_t mid = (lo_b + hi) >> 1;
+        const bool okm = tile8_sum(vals.count_ge(mid)) >= mid;
+        if (hi - lo_b > 1) {
+          if (okm) lo_b = mid; else hi = mid;
+        }
+      }
+      const uint32_t t = cA >= cap ? cap : lo_b;
+      const uint32_t c = tile8_sum(vals.count_ge(t));
+      if (has && k == 0) {
+        Item it;
+        it.u = u; it.cap = cap; it.deg = deg; it.len = deg; it.thr = 0;
+        finish_eval(p, it, t, c, deg, acc);
+      }
+    }
+  });
+}
+
+// THREAD class (deg <= 8): thread per vertex, h = max_i min(x_i, #{x_j >= x_i}).
+template <typename OffT, typename EstT>
+__device__ __noinline__ void eval_thread(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                            Acc& acc) {
+  constexpr int R = DEG_THREAD_MAX;
+  const EstT* snap = v.snap;
+  const uint32_t cache_n = v.cache_n;
+  for_class(p, v, C_THREAD, GMAX_SMALL, [&](uint32_t u, uint32_t n) {
+    if (lane_id() >= n) return;
+    const uint64_t ob = p.off[u];
+    const uint32_t deg = (uint32_t)(p.off[u + 1] - ob);
+    const uint32_t cap = est_at(s_cache, cache_n, snap, u);
+    uint32_t x[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const uint32_t id = (uint32_t)j < deg ? p.adj[ob + j] : 0xffffffffu;
+      x[j] = id != 0xffffffffu ? est_at(s_cache, cache_n, snap, id) : 0u;
+    }
+    uint32_t h = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int j = 0; j < R; ++j) c += x[j] >= x[i];
+      const uint32_t m = x[i] < c ? x[i] : c;
+      h = m > h ? m : h;
+    }
+    const uint32_t t = h < cap ? h : cap;
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) c += x[j] >= t;
+    Item it;
+    it.u = u; it.cap = cap; it.deg = deg; it.len = deg; it.thr = 0;
+    finish_eval(p, it, t, t ? c : deg, deg, acc);
+  });
+}
+
+// ------------------------------------------------------------------------
+// NOTIFY.  A dropper scans its list (or its CSR row, building the list when
+// the row is longer than LIST_MIN_DEG) against the settled values N.
+// ------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t list_threshold(uint32_t t) {
+  const uint32_t L = t - (t >> KC_LIST_SHIFT);
+  return L ? L : 1u;
+}
+
+template <bool RO, typename OffT, typename EstT>
+__device__ __noinline__ void notify_warp(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                         const EstT* s_cache, uint32_t* wbuf, uint32_t* wn,
+                                         const uint32_t* src, uint32_t u, uint64_t ob,
+                                         uint32_t len, uint32_t t, uint32_t cap, uint32_t build,
+                                         Acc& acc) {
+  uint32_t cursor = 0;  // warp-uniform
+  const uint32_t cache_n = v.cache_n;
+  stream_row<32, RO>(src, p.N, lane_id(), ob, ob + len, s_cache, cache_n,
+                     [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
+                       notify8(p, v, wbuf, wn, ok, ids, x, t, cap, acc);
+                       if (build) {
+                         uint32_t keep = 0;
+#pragma unroll
+                         for (int k = 0; k < 8; ++k) keep |= (uint32_t)((ok >> k & 1) && x[k] >= build) << k;
+                         const uint32_t nk = __popc(keep);
+                         const uint32_t incl = warp_incl_scan(nk);
+                         uint32_t pos = cursor + incl - nk;
+#pragma unroll
+                         for (int k = 0; k < 8; ++k)
+                           if (keep >> k & 1) p.radj[ob + pos++] = ids[k];
+                         cursor += __shfl_sync(FULL, incl, 31);
+                       }
+                     });
+  if (lane_id() == 0) {
+    acc.nscan += len;
+    if (build) {
+      p.rlen[u] = cursor;
+      p.rthr[u] = (EstT)build;
+    }
+    p.E[u] = (EstT)t;  // apply (fastk.cpp:153)
+  }
+}
+
+template <bool RO, typename OffT, typename EstT>
+__device__ __noinline__ void notify_cta(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                        const EstT* s_cache, uint32_t* wbuf, uint32_t* wn,
+                                        Shared& sh, const uint32_t* src, uint32_t u, uint64_t ob,
+                                        uint32_t len, uint32_t t, uint32_t cap, uint32_t build,
+                                        Acc& acc) {
+  if (threadIdx.x == 0) sh.cursor = 0;
+  __syncthreads();
+  const uint32_t cache_n = v.cache_n;
+  stream_row<SOLVE_THREADS, RO>(src, p.N, threadIdx.x, ob, ob + len, s_cache, cache_n,
+                                [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
+                                  notify8(p, v, wbuf, wn, ok, ids, x, t, cap, acc);
+                                  if (build) {
+                                    uint32_t keep = 0;
+#pragma unroll
+                                    for (int k = 0; k < 8; ++k)
+                                      keep |= (uint32_t)((ok >> k & 1) && x[k] >= build) << k;
+                                    const uint32_t nk = __popc(keep);
+                                    const uint32_t incl = warp_incl_scan(nk);
+                                    const uint32_t tot = __shfl_sync(FULL, incl, 31);
+                                    uint32_t base = 0;
+                                    if (lane_id() == 0 && tot) base = atomicAdd(&sh.cursor, tot);
+                                    uint32_t pos = __shfl_sync(FULL, base, 0) + incl - nk;
+#pragma unroll
+                                    for (int k = 0; k < 8; ++k)
+                                      if (keep >> k & 1) p.radj[ob + pos++] = ids[k];
+                                  }
+                                });
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    acc.nscan += len;
+    if (build) {
+      p.rlen[u] = sh.cursor;
+      p.rthr[u] = (EstT)build;
+    }
+    p.E[u] = (EstT)t;
+  }
+  __syncthreads();
+}
+
+struct Drop {
+  uint32_t u, t, cap, thr, len, deg;
+  uint64_t ob;
+};
+
+template <typename OffT, typename EstT>
+__device__ __forceinline__ Drop drop_item(const CP<OffT, EstT>& p, uint32_t u) {
+  Drop d;
+  d.u = u;
+  d.t = p.N[u];
+  d.cap = p.E[u];
+  d.ob = p.off[u];
+  d.deg = (uint32_t)(p.off[u + 1] - d.ob);
+  d.thr = 0;
+  d.len = d.deg;
+  if (d.t < d.cap && d.deg > LIST_MIN_DEG) {
+    d.thr = p.rthr[u];
+    if (d.thr) d.len = p.rlen[u];
+  }
+  return d;
+}
+
+template <typename OffT, typename EstT>
+__device__ __forceinline__ void notify_drop_warp(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                                 const EstT* s_cache, uint32_t* wbuf, uint32_t* wn,
+                                                 const Drop& d, Acc& acc) {
+  if (d.thr)  // in place: drop entries whose settled value fell below the threshold
+    notify_warp<false>(p, v, s_cache, wbuf, wn, p.radj, d.u, d.ob, d.len, d.t, d.cap,
+                       KC_LIST_COMPACT ? d.thr : 0u, acc);
+  else
+    notify_warp<true>(p, v, s_cache, wbuf, wn, p.adj, d.u, d.ob, d.len, d.t, d.cap,
+                      (!v.r0 && d.deg > LIST_MIN_DEG) ? list_threshold(d.t) : 0u, acc);
+}
+
+template <typename OffT, typename EstT>
+__device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                              uint32_t* wbuf, uint32_t* wn, int c, uint32_t gmax, Acc& acc) {
+  for_class(p, v, c, gmax, [&](uint32_t u, uint32_t n) {
+    Drop mine{};
+    if (lane_id() < n) mine = drop_item(p, u);
+    for (uint32_t i = 0; i < n; ++i) {
+      Drop d;
+      d.t = __shfl_sync(FULL, mine.t, i);
+      d.cap = __shfl_sync(FULL, mine.cap, i);
+      if (d.t >= d.cap) continue;  // round 0: evaluated, no drop (warp-uniform)
+      d.u = __shfl_sync(FULL, mine.u, i);
+      d.thr = __shfl_sync(FULL, mine.thr, i);
+      d.len = __shfl_sync(FULL, mine.len, i);
+      d.deg = __shfl_sync(FULL, mine.deg, i);
+      d.ob = __shfl_sync(FULL, mine.ob, i);
+      notify_drop_warp(p, v, s_cache, wbuf, wn, d, acc);
+    }
+  });
+}
+
+// SUB and THREAD droppers: 8-lane tile per dropper, up to 8 neighbours per lane.
+template <typename OffT, typename EstT>
+__device__ __noinline__ void notify_small(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                             uint32_t* wbuf, uint32_t* wn, int c, Acc& acc) {
+  const uint32_t g = lane_id() >> 3, k = lane_id() & 7;
+  const uint32_t cache_n = v.cache_n;
+  for_class(p, v, c, GMAX_SMALL, [&](uint32_t mu, uint32_t n) {
+    for (uint32_t i0 = 0; i0 < n; i0 += 4) {
+      const uint32_t u = __shfl_sync(FULL, mu, (int)(i0 + g) & 31);
+      uint32_t t = 0, cap = 0, deg = 0;
+      uint64_t ob = 0;
+      if (i0 + g < n) {
+        t = p.N[u];
+        cap = p.E[u];
+        if (t < cap) {
+          ob = p.off[u];
+          deg = (uint32_t)(p.off[u + 1] - ob);
+        }
+      }
+      uint32_t ids[8], x[8], ok = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool val = k + 8u * j < deg;
+        ids[j] = val ? p.adj[ob + k + 8u * j] : 0u;
+        ok |= (uint32_t)val << j;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        x[j] = (ok >> j & 1) ? est_at(s_cache, cache_n, (const EstT*)p.N, ids[j]) : 0u;
+      notify8(p, v, wbuf, wn, ok, ids, x, t, cap, acc);  // warp-converged
+      if (k == 0 && t < cap) {
+        acc.nscan += deg;
+        p.E[u] = (EstT)t;
+      }
+    }
+  });
+}
+
+template <typename OffT, typename EstT>
+__device__ __forceinline__ void flush_acc(const CP<OffT, EstT>& p, uint32_t sr, const Acc& acc,
+                                          unsigned long long* s_acc) {
+  const unsigned long long val[6] = {acc.evals, acc.escan, acc.drops, acc.fires, acc.nscan, acc.ascan};
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    unsigned long long x = val[q];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(FULL, x, d);
+    if (lane_id() == 0 && x) atomicAdd(&s_acc[q], x);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    RoundStat& st = p.stats[sr];
+    unsigned long long* dst[6] = {&st.evals, &st.escan, &st.drops, &st.fires, &st.nscan, &st.ascan};
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+      if (s_acc[q]) atomicAdd(dst[q], s_acc[q]);
+  }
+}
+
+template <typename OffT, typename EstT>
+__global__ void __launch_bounds__(SOLVE_THREADS, 1) count_kernel(const __grid_constant__ CP<OffT, EstT> p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem[];
+  EstT* s_cache = reinterpret_cast<EstT*>(smem);
+  const size_t cache_bytes = ((size_t)p.cache_n * sizeof(EstT) + 15) & ~(size_t)15;
+  uint32_t* s_hist = reinterpret_cast<uint32_t*>(smem + cache_bytes);  // CTA window / warp bins
+  uint32_t* w_bins = s_hist + WARP_BINS * warp_id();
+  uint32_t* s_wq = s_hist + HIST_BINS;  // per-warp enqueue buffers
+  uint32_t* wbuf = s_wq + (size_t)warp_id() * NCLS * WQ;
+  __shared__ uint32_t s_wn[NWARPS][NCLS];
+  __shared__ Shared sh;
+  uint32_t* wn = s_wn[warp_id()];
+  const uint32_t tid = threadIdx.x;
+  if (tid == 0) sh.ticket = 0xffffffffu;
+  if (lane_id() < NCLS) wn[lane_id()] = 0;
+  __syncthreads();
+
+  for (uint32_t r = p.r_begin; r < p.r_end; ++r) {
+    const uint32_t cur = r & 1, nxt = cur ^ 1;
+    const uint32_t sr = r < STAT_SLOTS - 1 ? r : STAT_SLOTS - 1;
+    View<EstT> v;
+    v.snap = p.E;
+    v.q = r == 0 ? nullptr : p.queue[cur];
+    v.qcnt = p.ctl[cur].qcnt;
+    v.grab = p.ctl[cur].grab;
+    v.qn = p.ctl[nxt].qcnt;
+    v.qnext = p.queue[nxt];
+    v.r0 = r == 0;
+    unsigned long long* pf = (p.prof && r < PROF_ROUNDS && tid == 0)
+                                 ? p.prof + ((size_t)r * gridDim.x + blockIdx.x) * PROF_PHASES
+                                 : nullptr;
+    if (pf) pf[0] = gtimer();
+    uint32_t active = 0;
+#pragma unroll
+    for (int c = 0; c < NCLS; ++c) active += v.qcnt[c];
+    if (r > 0 && active == 0) {  // quiescent round: converged (fastk.cpp:109-110)
+      if (blockIdx.x == 0 && tid == 0) {
+        p.status[0] = r + 1;
+        p.status[1] = 1;
+        p.status[3] = 0;
+      }
+      if (pf) pf[1] = pf[2] = pf[3] = pf[4] = pf[5] = pf[6] = pf[7] = gtimer();
+      return;
+    }
+    // the next round's queue sizes and cursors (idle until the notify phase)
+    if (blockIdx.x == 0 && tid < NCLS) {
+      p.ctl[nxt].grab[tid] = 0;
+      p.ctl[nxt].grab2[tid] = 0;
+      p.ctl[nxt].qcnt[tid] = 0;
+      if (tid < 2) p.ctl[nxt].lqn[tid] = p.ctl[nxt].lqc[tid] = p.ctl[nxt].lqd[tid] = 0;
+    }
+    if (blockIdx.x == 0 && tid == 32) {
+      p.stats[sr].q01 = v.qcnt[0] | (unsigned long long)v.qcnt[1] << 32;
+      p.stats[sr].q23 = v.qcnt[2] | (unsigned long long)v.qcnt[3] << 32;
+      p.stats[sr].q4 = v.qcnt[4];
+    }
+    if (tid < 6) sh.acc[tid] = 0;
+    if (tid == 0) sh.drop = 0;
+    const uint32_t cache_n = active >= CACHE_MIN_ACTIVE ? p.cache_n : 0u;
+    v.cache_n = cache_n;
+    if (cache_n) fill_cache(s_cache, (const EstT*)p.E, cache_n);
+    __syncthreads();
+    Acc acc{0, 0, 0, 0, 0, 0, false};
+    if (pf) pf[1] = gtimer();
+    // ---------------- EVALUATE ----------------
+    Ctl& ctl = p.ctl[cur];
+    auto eval_long = [&](uint32_t u) { eval_cta(p, v, s_cache, s_hist, sh, u, acc); };
+    huge_warps(
+        p, v, sh, ctl, 0,
+        [&](uint32_t u) { return eval_item(p, v, s_cache, u).len > WARP_MAX_LEN; },
+        [&](uint32_t u) {
+          const Item it = eval_item(p, v, s_cache, u);
+          eval_warp(p, v, s_cache, w_bins, it, acc);
+        });
+    consume_long(p, v, sh, ctl, 0, false, eval_long);
+    if (pf) pf[2] = gtimer();
+    eval_wclass(p, v, s_cache, w_bins, C_BIG, GMAX_BIG, acc);
+    eval_wclass(p, v, s_cache, w_bins, C_WARP, GMAX_WARP, acc);
+    if (pf) pf[3] = gtimer();
+    eval_sub(p, v, s_cache, acc);
+    eval_thread(p, v, s_cache, acc);
+    consume_long(p, v, sh, ctl, 0, true, eval_long);
+    if (pf) pf[4] = gtimer();
+    if (v.r0) {
+      if (__any_sync(FULL, acc.any_drop) && lane_id() == 0) sh.drop = 1;
+      __syncthreads();
+      if (tid == 0 && sh.drop) p.anydrop[0] = 1;
+    }
+    grid.sync();
+    // The reference starts at est = deg (fastk.cpp:67-68); the solver starts
+    // at min(deg, H), so round 0 "changed" also when some degree exceeds H
+    // (that drop is already applied).  Keeps iterations equal to the reference.
+    if (v.r0 && !(*reinterpret_cast<volatile uint32_t*>(&p.anydrop[0]) != 0 || p.clamp_drop)) {
+      flush_acc(p, sr, acc, sh.acc);
+      if (blockIdx.x == 0 && tid == 0) {
+        p.status[0] = 1;
+        p.status[1] = 1;
+        p.status[3] = 0;
+      }
+      if (pf) pf[5] = pf[6] = pf[7] = gtimer();
+      return;
+    }
+    if (pf) pf[5] = gtimer();
+    // ---------------- NOTIFY + APPLY ----------------
+    v.snap = p.N;
+    v.grab = p.ctl[cur].grab2;
+    if (cache_n) fill_cache(s_cache, (const EstT*)p.N, cache_n);
+    __syncthreads();
+    if (pf) pf[6] = gtimer();
+    auto notify_long = [&](uint32_t u) {
+      const Drop d = drop_item(p, u);  // a long-queued hub always dropped
+      if (d.thr)
+        notify_cta<false>(p, v, s_cache, wbuf, wn, sh, p.radj, d.u, d.ob, d.len, d.t, d.cap, 0u,
+                          acc);
+      else
+        notify_cta<true>(p, v, s_cache, wbuf, wn, sh, p.adj, d.u, d.ob, d.len, d.t, d.cap,
+                         v.r0 ? 0u : list_threshold(d.t), acc);
+    };
+    huge_warps(
+        p, v, sh, ctl, 1,
+        [&](uint32_t u) {
+          const Drop d = drop_item(p, u);
+          return d.t < d.cap && d.len > WARP_MAX_LEN;
+        },
+        [&](uint32_t u) {
+          const Drop d = drop_item(p, u);
+          if (d.t < d.cap) notify_drop_warp(p, v, s_cache, wbuf, wn, d, acc);
+        });
+    consume_long(p, v, sh, ctl, 1, false, notify_long);
+    notify_wclass(p, v, s_cache, wbuf, wn, C_BIG, GMAX_BIG, acc);
+    notify_wclass(p, v, s_cache, wbuf, wn, C_WARP, GMAX_WARP, acc);
+    notify_small(p, v, s_cache, wbuf, wn, C_SUB, acc);
+    notify_small(p, v, s_cache, wbuf, wn, C_THREAD, acc);
+    consume_long(p, v, sh, ctl, 1, true, notify_long);
+#pragma unroll 1
+    for (int c = 0; c < NCLS; ++c) wq_flush(p, v, wbuf, wn, c);
+    flush_acc(p, sr, acc, sh.acc);
+    grid.sync();
+    if (pf) pf[7] = gtimer();
+    if (blockIdx.x == 0 && tid == 0) {
+      p.status[0] = r + 1;
+      p.status[3] = 0;
+    }
+  }
+}
+
+// Round-0 state: E = N = min(deg, H), no lists, the round-0
+// "queue" is every vertex (class sizes), everything else cleared.
+template <typename OffT, typename EstT>
+__global__ void count_init_kernel(CP<OffT, EstT> p, uint32_t h_graph, uint32_t n_pad) {
+  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t gsize = gridDim.x * blockDim.x;
+  for (uint32_t u = gtid; u < n_pad; u += gsize) {
+    EstT e = 0;
+    if (u < p.n_nz) {
+      const uint32_t d = (uint32_t)(p.off[u + 1] - p.off[u]);
+      e = (EstT)(d < h_graph ? d : h_graph);
+    }
+    p.E[u] = e;
+    p.N[u] = e;
+    p.cnt[u] = 0;
+    p.rthr[u] = 0;
+  }
+  for (uint32_t k = gtid; k < STAT_SLOTS * (uint32_t)(sizeof(RoundStat) / 8); k += gsize)
+    reinterpret_cast<unsigned long long*>(p.stats)[k] = 0;
+  if (gtid < NCLS) {
+    p.ctl[0].grab[gtid] = p.ctl[0].grab2[gtid] = 0;
+    p.ctl[0].qcnt[gtid] = p.cb[gtid + 1] - p.cb[gtid];
+    p.ctl[1].grab[gtid] = p.ctl[1].grab2[gtid] = p.ctl[1].qcnt[gtid] = 0;
+  }
+  if (gtid < 2)
+    for (int q = 0; q < 2; ++q) p.ctl[q].lqn[gtid] = p.ctl[q].lqc[gtid] = p.ctl[q].lqd[gtid] = 0;
+  if (gtid < 3) p.anydrop[gtid] = 0;
+  if (gtid < 4) p.status[gtid] = 0;
+}
+
+template <typename OffT, typename EstT>
+CP<OffT, EstT> make_params(const SolveBuffers& b) {
+  CP<OffT, EstT> p{};
+  p.off = static_cast<const OffT*>(b.off);
+  p.adj = b.adj;
+  p.radj = b.radj;
+  p.rlen = b.rlen;
+  p.rthr = static_cast<EstT*>(b.rthr);
+  p.n_nz = b.n_nz;
+  for (int c = 0; c <= NCLS; ++c) p.cb[c] = b.cls_begin[c];
+  p.E = static_cast<EstT*>(b.est[0]);
+  p.N = static_cast<EstT*>(b.est[1]);
+  p.cnt = b.cnt;
+  p.queue[0] = b.queue;
+  p.queue[1] = b.queue2;
+  p.lq[0] = b.lq[0];
+  p.lq[1] = b.lq[1];
+  p.ctl = b.ctl;
+  p.anydrop = b.anydrop;
+  p.stats = b.stats;
+  p.status = b.status;
+  p.prof = b.prof;
+  return p;
+}
+
+template <typename OffT, typename EstT>
+cudaError_t launch_t(const SolveBuffers& b, const SolveConfig& c, uint32_t r_begin, uint32_t r_end,
+                     cudaStream_t stream) {
+  CP<OffT, EstT> p = make_params<OffT, EstT>(b);
+  p.r_begin = r_begin;
+  p.r_end = r_end;
+  p.cache_n = c.cache_n;
+  p.clamp_drop = c.clamp_drop;
+  const size_t smem = (((size_t)c.cache_n * sizeof(EstT) + 15) & ~(size_t)15) +
+                      ((size_t)HIST_BINS + (size_t)NWARPS * NCLS * WQ) * sizeof(uint32_t);
+  static_assert(HIST_BINS >= (int)NWARPS * WARP_BINS, "warp bins alias the CTA histogram");
+  auto kern = count_kernel<OffT, EstT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SOLVE_THREADS, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  dim3 grid(c.num_sms), block(SOLVE_THREADS);
+  void* args[] = {&p};
+  return cudaLaunchCooperativeKernel((const void*)kern, grid, block, args, smem, stream);
+}
+
+template <typename OffT, typename EstT>
+cudaError_t init_t(const SolveBuffers& b, uint32_t h_graph, cudaStream_t stream) {
+  CP<OffT, EstT> p = make_params<OffT, EstT>(b);
+  const uint32_t n_pad = (b.n_nz + 15) & ~15u;
+  count_init_kernel<OffT, EstT><<<148 * 4, 256, 0, stream>>>(p, h_graph, n_pad);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_count_rounds(const SolveBuffers& b, const SolveConfig& c, bool est16, bool off64,
+                                uint32_t r_begin, uint32_t r_end, cudaStream_t stream) {
+  if (est16)
+    return off64 ? launch_t<uint64_t, uint16_t>(b, c, r_begin, r_end, stream)
+                 : launch_t<uint32_t, uint16_t>(b, c, r_begin, r_end, stream);
+  return off64 ? launch_t<uint64_t, uint32_t>(b, c, r_begin, r_end, stream)
+               : launch_t<uint32_t, uint32_t>(b, c, r_begin, r_end, stream);
+}
+
+cudaError_t launch_count_init(const SolveBuffers& b, bool est16, bool off64, uint32_t h_graph,
+                              cudaStream_t stream) {
+  if (est16)
+    return off64 ? init_t<uint64_t, uint16_t>(b, h_graph, stream)
+                 : init_t<uint32_t, uint16_t>(b, h_graph, stream);
+  return off64 ? init_t<uint64_t, uint32_t>(b, h_graph, stream)
+               : init_t<uint32_t, uint32_t>(b, h_graph, stream);
+}
+
+}  // namespace kcb

@@ -1,0 +1,281 @@
+// kc_dev.cuh — device building blocks shared by the two solvers:
+// kc_solve.cu (reference activation rule, byte-flag frontier) and
+// kc_count.cu (counting rule, direct queues, relevant-neighbour lists).
+//
+// The h-index pieces restate include/kcore/kernel.hpp:27-42
+// (compute_index_over): values are capped at `cap`, counted per level, and
+// the answer is the largest level t >= 1 with count(>= t) >= t.
+#pragma once
+#include <cstdint>
+
+#include "kc_internal.h"
+
+namespace kcb {
+namespace dev {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint32_t NWARPS = SOLVE_THREADS / 32;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }
+__device__ __forceinline__ uint32_t lanemask_lt() { return (1u << lane_id()) - 1u; }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Estimate of v: shared-memory cache for the highest-degree ids, global
+// (L1/L2) otherwise.  One generic load per gather keeps the inlined gather
+// sites small for the instruction cache.
+template <typename EstT>
+__device__ __forceinline__ uint32_t est_at(const EstT* __restrict__ s_cache, uint32_t cache_n,
+                                           const EstT* snap, uint32_t v) {
+  const EstT* base = v < cache_n ? s_cache : snap;
+  return (uint32_t)base[v];
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, v, d);
+    if (lane >= (uint32_t)d) v += y;
+  }
+  return v;
+}
+
+// ------------------------------------------------------------------------
+// Values held in registers: R per lane.  16-bit estimates are < 2^15
+// (EST16_LIMIT), so two share a register and "x >= t" for both halves is
+// one OR + one subtract: the top bit of ((x | 0x8000) - t) is set iff x >= t.
+// ------------------------------------------------------------------------
+template <typename EstT, int R>
+struct Vals;
+
+template <int R>
+struct Vals<uint16_t, R> {
+  static_assert(R % 2 == 0, "pairs");
+  uint32_t w[R / 2];
+  __device__ __forceinline__ void clear() {
+#pragma unroll
+    for (int j = 0; j < R / 2; ++j) w[j] = 0;
+  }
+  __device__ __forceinline__ void set(int j, uint32_t x) {
+    if (j & 1) w[j >> 1] |= x << 16; else w[j >> 1] |= x;
+  }
+  __device__ __forceinline__ uint32_t get(int j) const {
+    return (j & 1) ? (w[j >> 1] >> 16) : (w[j >> 1] & 0xffffu);
+  }
+  __device__ __forceinline__ uint32_t count_ge(uint32_t t) const {
+    const uint32_t tt = t | (t << 16);
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < R / 2; ++j) c += __popc(((w[j] | 0x80008000u) - tt) & 0x80008000u);
+    return c;
+  }
+};
+
+template <int R>
+struct Vals<uint32_t, R> {
+  uint32_t w[R];
+  __device__ __forceinline__ void clear() {
+#pragma unroll
+    for (int j = 0; j < R; ++j) w[j] = 0;
+  }
+  __device__ __forceinline__ void set(int j, uint32_t x) { w[j] = x; }
+  __device__ __forceinline__ uint32_t get(int j) const { return w[j]; }
+  __device__ __forceinline__ uint32_t count_ge(uint32_t t) const {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) c += w[j] >= t;
+    return c;
+  }
+};
+
+// 128-bit load of the 4 neighbour ids at aligned position a (multiple of 4).
+// RO: the array is immutable for the kernel's lifetime (the CSR) — non-
+// coherent path, no L1 allocation (L1 is left to the estimate gathers).
+// Otherwise (lists rewritten inside the kernel): L2 only.
+template <bool RO>
+__device__ __forceinline__ uint4 ld_ids4(const uint32_t* src, uint64_t a) {
+  uint4 r;
+  if (RO)
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(src + a));
+  else
+    asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(src + a));
+  return r;
+}
+__device__ __forceinline__ uint32_t u4_get(const uint4& q, int e) {
+  return e == 0 ? q.x : e == 1 ? q.y : e == 2 ? q.z : q.w;
+}
+
+// ------------------------------------------------------------------------
+// Block-wide helpers (blockDim == SOLVE_THREADS)
+// ------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* s_red) {
+  v = __reduce_add_sync(FULL, v);
+  if (lane_id() == 0) s_red[warp_id()] = v;
+  __syncthreads();
+  if (warp_id() == 0) {
+    uint32_t w = __reduce_add_sync(FULL, lane_id() < NWARPS ? s_red[lane_id()] : 0u);
+    if (lane_id() == 0) s_red[32] = w;
+  }
+  __syncthreads();
+  return s_red[32];
+}
+
+__device__ __forceinline__ uint32_t block_min(uint32_t v, uint32_t* s_red) {
+  v = __reduce_min_sync(FULL, v);
+  if (lane_id() == 0) s_red[warp_id()] = v;
+  __syncthreads();
+  if (warp_id() == 0) {
+    uint32_t w = __reduce_min_sync(FULL, lane_id() < NWARPS ? s_red[lane_id()] : 0xffffffffu);
+    if (lane_id() == 0) s_red[32] = w;
+  }
+  __syncthreads();
+  return s_red[32];
+}
+
+// Exclusive prefix sum over the block (thread order).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_red) {
+  const uint32_t incl = warp_incl_scan(v);
+  if (lane_id() == 31) s_red[warp_id()] = incl;
+  __syncthreads();
+  if (warp_id() == 0) {
+    const uint32_t w = lane_id() < NWARPS ? s_red[lane_id()] : 0u;
+    const uint32_t e = warp_incl_scan(w) - w;
+    if (lane_id() < NWARPS) s_red[lane_id()] = e;
+  }
+  __syncthreads();
+  const uint32_t r = s_red[warp_id()] + incl - v;
+  __syncthreads();
+  return r;
+}
+
+// Tally one gathered value into the window [top - NB, top): bin i counts
+// x == top-1-i, `above` counts x >= top (the capped top bin of
+// compute_index_over, kernel.hpp:31-35, kept in registers).
+// Values below `floor` cannot change the answer (it is known to be >= floor)
+// and are skipped.
+template <int NB>
+__device__ __forceinline__ void tally(uint32_t x, uint32_t top, uint32_t floor, uint32_t& above,
+                                      uint32_t* bins) {
+  if (x >= top) ++above;
+  else if ((int)x >= (int)top - NB && x >= floor) atomicAdd(&bins[top - 1 - x], 1u);
+}
+
+// Suffix scan of one window (kernel.hpp:36-41): the smallest bin i whose
+// level x = top-1-i >= minlvl (>= 1) has count(>= x) = C + sum(bins[0..i])
+// >= x.  Levels below the tally floor are not complete, so minlvl must be
+// >= the floor.  Warp version, lane l owns bins [8l, 8l+8).  Returns the
+// level and, in `cnt`, count(>= level).
+__device__ __forceinline__ bool warp_resolve(const uint32_t* bins, uint32_t C, uint32_t top,
+                                             uint32_t& level, uint32_t& cnt,
+                                             uint32_t minlvl = 1) {
+  static_assert(WARP_BINS == 256, "8 bins per lane");
+  const uint32_t lane = lane_id();
+  const uint4 b0 = reinterpret_cast<const uint4*>(bins)[2 * lane];
+  const uint4 b1 = reinterpret_cast<const uint4*>(bins)[2 * lane + 1];
+  const uint32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += b[j];
+  uint32_t run = C + warp_incl_scan(s) - s;
+  uint32_t found = 0xffffffffu, frun = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    run += b[j];
+    const int i = (int)lane * 8 + j;
+    const int x = (int)top - 1 - i;
+    if (found == 0xffffffffu && x >= (int)minlvl && run >= (uint32_t)x) {
+      found = (uint32_t)i;
+      frun = run;
+    }
+  }
+  const uint32_t g = __reduce_min_sync(FULL, found);
+  if (g == 0xffffffffu) return false;
+  cnt = __shfl_sync(FULL, frun, g >> 3);
+  level = top - 1 - g;
+  return true;
+}
+
+__device__ __forceinline__ void warp_zero_bins(uint32_t* bins) {
+  const uint32_t lane = lane_id();
+  reinterpret_cast<uint4*>(bins)[2 * lane] = make_uint4(0, 0, 0, 0);
+  reinterpret_cast<uint4*>(bins)[2 * lane + 1] = make_uint4(0, 0, 0, 0);
+  __syncwarp();
+}
+
+__device__ __forceinline__ uint32_t tile8_sum(uint32_t v) {
+  v += __shfl_xor_sync(FULL, v, 4, 8);
+  v += __shfl_xor_sync(FULL, v, 2, 8);
+  v += __shfl_xor_sync(FULL, v, 1, 8);
+  return v;
+}
+
+// ------------------------------------------------------------------------
+// Streaming over a row with 128-bit id loads: each of NT cooperating threads
+// takes 8 entries per step (two 16-byte loads, software-pipelined one step
+// ahead), gathers their 8 estimates, then hands (valid mask, ids, estimates)
+// to the callback.  Rows need not be 16-byte aligned: positions outside
+// [ob, oe) are masked (id arrays have ADJ_PAD spare entries).
+// ------------------------------------------------------------------------
+template <int NT, bool RO, typename EstT, typename F>
+__device__ __forceinline__ void stream_row(const uint32_t* src, const EstT* snap, uint32_t me,
+                                           uint64_t ob, uint64_t oe, const EstT* s_cache,
+                                           uint32_t cache_n, F&& f) {
+  constexpr uint64_t STEP = (uint64_t)NT * 8;
+  uint64_t a = ob & ~(uint64_t)3;
+  uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
+  if (a + 4 * me < oe) q0 = ld_ids4<RO>(src, a + 4 * me);
+  if (a + 4 * me + 4 * NT < oe) q1 = ld_ids4<RO>(src, a + 4 * me + 4 * NT);
+  for (; a < oe; a += STEP) {
+    uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
+    const uint64_t nb = a + STEP;
+    if (nb + 4 * me < oe) n0 = ld_ids4<RO>(src, nb + 4 * me);
+    if (nb + 4 * me + 4 * NT < oe) n1 = ld_ids4<RO>(src, nb + 4 * me + 4 * NT);
+    uint32_t ids[8], x[8];
+    uint32_t ok = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint64_t pos = a + 4 * me + (k >> 2) * 4 * NT + (k & 3);
+      ids[k] = u4_get(k < 4 ? q0 : q1, k & 3);
+      const bool v = pos >= ob && pos < oe;
+      ok |= (uint32_t)v << k;
+      x[k] = v ? est_at(s_cache, cache_n, snap, ids[k]) : 0u;
+    }
+    f(ok, ids, x);
+    q0 = n0;
+    q1 = n1;
+  }
+}
+
+template <typename EstT>
+__device__ __forceinline__ void fill_cache(EstT* s_cache, const EstT* src, uint32_t cache_n) {
+  // cache_n * sizeof(EstT) is a multiple of 16 bytes; 8 loads in flight per
+  // thread so the fill costs ~2 memory round trips, not nvec / SOLVE_THREADS
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(s_cache);
+  const uint32_t nvec = (uint32_t)((size_t)cache_n * sizeof(EstT) / 16);
+  for (uint32_t i0 = threadIdx.x; i0 < nvec; i0 += 8 * SOLVE_THREADS) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t i = i0 + k * SOLVE_THREADS;
+      if (i < nvec) v[k] = s[i];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t i = i0 + k * SOLVE_THREADS;
+      if (i < nvec) d[i] = v[k];
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace kcb

@@ -36,13 +36,20 @@ struct Ctl {                 // per round parity
   uint32_t grab[NCLS];       // evaluate phase cursors, per class
   uint32_t grab2[NCLS];      // notify phase cursors, per class
   uint32_t qcnt[NCLS];       // active vertices of each class (compacted queue)
-  uint32_t pad[1];
+  uint32_t lqn[2], lqc[2], lqd[2];  // counting solver: long-scan queue per phase —
+                                    // appended, consumed, CTAs done appending
+  uint32_t pad[3];
 };
 
 constexpr uint32_t STAT_SLOTS = 4096;  // rounds >= STAT_SLOTS-1 share the last slot
 
 struct RoundStat {           // per round, accumulated with atomics
-  unsigned long long evals, escan, drops, fires, pad0, pad1, pad2, pad3;
+  unsigned long long evals;  // vertex evaluations
+  unsigned long long escan;  // sum of degrees over evaluations (E_scan)
+  unsigned long long drops, fires;
+  unsigned long long nscan;  // entries streamed by the notify phase
+  unsigned long long ascan;  // entries streamed by the evaluate phase (lists: < escan)
+  unsigned long long q01, q23, q4;  // queue sizes: HUGE | BIG<<32, WARP | SUB<<32, THREAD
 };
 
 struct SolveBuffers {
@@ -58,6 +65,11 @@ struct SolveBuffers {
   uint32_t* cnt;             // R_COUNT: #neighbours w with est_w >= est_v [n_pad]
   uint8_t* flag[2];          // frontier byte flags; flag[r & 1] = round r's active set
   uint32_t* queue;           // [n_pad] round r's active ids, class c segment at cls_begin[c]
+  uint32_t* queue2;          // counting rule: the other round parity's queue [n_pad]
+  uint32_t* radj;            // counting rule: relevant-neighbour lists [nnz + ADJ_PAD]
+  uint32_t* rlen;            // counting rule: list lengths [n_pad]
+  void* rthr;                // counting rule: list thresholds (EstT) [n_pad]
+  uint32_t* lq[2];           // counting rule: long-scan queues per phase [cls_begin[1]]
   Ctl* ctl;                  // [2]
   uint32_t* anydrop;         // [3] "some estimate dropped in round r" (r % 3)
   RoundStat* stats;          // [STAT_SLOTS]
@@ -81,6 +93,11 @@ struct SolveConfig {
 // est16: estimates are uint16 (else uint32); off64: offsets are uint64.
 cudaError_t launch_rounds(const SolveBuffers& b, const SolveConfig& c, bool est16, bool off64,
                           uint32_t r_begin, uint32_t r_end, cudaStream_t stream);
+// The counting-rule solver (kc_count.cu): same contract.
+cudaError_t launch_count_rounds(const SolveBuffers& b, const SolveConfig& c, bool est16, bool off64,
+                                uint32_t r_begin, uint32_t r_end, cudaStream_t stream);
+cudaError_t launch_count_init(const SolveBuffers& b, bool est16, bool off64, uint32_t h_graph,
+                              cudaStream_t stream);
 // Initialise estimates (min(deg, H)), round-0 frontier, counters.
 cudaError_t launch_init(const SolveBuffers& b, bool est16, bool off64, uint32_t h_graph,
                         uint32_t max_rounds, cudaStream_t stream);

@@ -36,15 +36,15 @@
 #include <cooperative_groups.h>
 #include <cstdint>
 
+#include "kc_dev.cuh"
 #include "kc_internal.h"
 
 namespace cg = cooperative_groups;
 
 namespace kcb {
 namespace {
+using namespace dev;
 
-constexpr unsigned FULL = 0xffffffffu;
-constexpr uint32_t NWARPS = SOLVE_THREADS / 32;
 // Active vertices grabbed per atomic, per class.
 constexpr uint32_t G_BIG = 2, G_WARP = 8, G_SUB = 32, G_THREAD = 32;
 constexpr uint32_t COMPACT_IDS = SOLVE_THREADS * 16;  // ids per CTA compaction block
@@ -89,226 +89,6 @@ struct Acc {  // per-thread counters, flushed per round
   unsigned long long evals, escan, drops, fires, nscan;
   bool any_drop;
 };
-
-__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
-__device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }
-__device__ __forceinline__ uint32_t lanemask_lt() { return (1u << lane_id()) - 1u; }
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-// Estimate of v: shared-memory cache for the highest-degree ids, global
-// (L1/L2) otherwise.  One generic load per gather keeps the inlined gather
-// sites small for the instruction cache.
-template <typename EstT>
-__device__ __forceinline__ uint32_t est_at(const EstT* __restrict__ s_cache, uint32_t cache_n,
-                                           const EstT* snap, uint32_t v) {
-  const EstT* base = v < cache_n ? s_cache : snap;
-  return (uint32_t)base[v];
-}
-
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
-  const uint32_t lane = lane_id();
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t y = __shfl_up_sync(FULL, v, d);
-    if (lane >= (uint32_t)d) v += y;
-  }
-  return v;
-}
-
-// ------------------------------------------------------------------------
-// Values held in registers: R per lane.  16-bit estimates are < 2^15
-// (EST16_LIMIT), so two share a register and "x >= t" for both halves is
-// one OR + one subtract: the top bit of ((x | 0x8000) - t) is set iff x >= t.
-// ------------------------------------------------------------------------
-template <typename EstT, int R>
-struct Vals;
-
-template <int R>
-struct Vals<uint16_t, R> {
-  static_assert(R % 2 == 0, "pairs");
-  uint32_t w[R / 2];
-  __device__ __forceinline__ void clear() {
-#pragma unroll
-    for (int j = 0; j < R / 2; ++j) w[j] = 0;
-  }
-  __device__ __forceinline__ void set(int j, uint32_t x) {
-    if (j & 1) w[j >> 1] |= x << 16; else w[j >> 1] |= x;
-  }
-  __device__ __forceinline__ uint32_t get(int j) const {
-    return (j & 1) ? (w[j >> 1] >> 16) : (w[j >> 1] & 0xffffu);
-  }
-  __device__ __forceinline__ uint32_t count_ge(uint32_t t) const {
-    const uint32_t tt = t | (t << 16);
-    uint32_t c = 0;
-#pragma unroll
-    for (int j = 0; j < R / 2; ++j) c += __popc(((w[j] | 0x80008000u) - tt) & 0x80008000u);
-    return c;
-  }
-};
-
-template <int R>
-struct Vals<uint32_t, R> {
-  uint32_t w[R];
-  __device__ __forceinline__ void clear() {
-#pragma unroll
-    for (int j = 0; j < R; ++j) w[j] = 0;
-  }
-  __device__ __forceinline__ void set(int j, uint32_t x) { w[j] = x; }
-  __device__ __forceinline__ uint32_t get(int j) const { return w[j]; }
-  __device__ __forceinline__ uint32_t count_ge(uint32_t t) const {
-    uint32_t c = 0;
-#pragma unroll
-    for (int j = 0; j < R; ++j) c += w[j] >= t;
-    return c;
-  }
-};
-
-// 128-bit load of the 4 neighbour ids at aligned position a (multiple of 4).
-// The adjacency is immutable for the kernel's lifetime: non-coherent path,
-// no L1 allocation (L1 is left to the estimate gathers).
-__device__ __forceinline__ uint4 ld_ids4(const uint32_t* adj, uint64_t a) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(adj + a));
-  return r;
-}
-__device__ __forceinline__ uint32_t u4_get(const uint4& q, int e) {
-  return e == 0 ? q.x : e == 1 ? q.y : e == 2 ? q.z : q.w;
-}
-
-// ------------------------------------------------------------------------
-// Block-wide helpers (blockDim == SOLVE_THREADS)
-// ------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* s_red) {
-  v = __reduce_add_sync(FULL, v);
-  if (lane_id() == 0) s_red[warp_id()] = v;
-  __syncthreads();
-  if (warp_id() == 0) {
-    uint32_t w = __reduce_add_sync(FULL, lane_id() < NWARPS ? s_red[lane_id()] : 0u);
-    if (lane_id() == 0) s_red[32] = w;
-  }
-  __syncthreads();
-  return s_red[32];
-}
-
-__device__ __forceinline__ uint32_t block_min(uint32_t v, uint32_t* s_red) {
-  v = __reduce_min_sync(FULL, v);
-  if (lane_id() == 0) s_red[warp_id()] = v;
-  __syncthreads();
-  if (warp_id() == 0) {
-    uint32_t w = __reduce_min_sync(FULL, lane_id() < NWARPS ? s_red[lane_id()] : 0xffffffffu);
-    if (lane_id() == 0) s_red[32] = w;
-  }
-  __syncthreads();
-  return s_red[32];
-}
-
-// Exclusive prefix sum over the block (thread order).
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_red) {
-  const uint32_t incl = warp_incl_scan(v);
-  if (lane_id() == 31) s_red[warp_id()] = incl;
-  __syncthreads();
-  if (warp_id() == 0) {
-    const uint32_t w = lane_id() < NWARPS ? s_red[lane_id()] : 0u;
-    const uint32_t e = warp_incl_scan(w) - w;
-    if (lane_id() < NWARPS) s_red[lane_id()] = e;
-  }
-  __syncthreads();
-  const uint32_t r = s_red[warp_id()] + incl - v;
-  __syncthreads();
-  return r;
-}
-
-// Tally one gathered value into the window [top - NB, top): bin i counts
-// x == top-1-i, `above` counts x >= top (the capped top bin of
-// compute_index_over, kernel.hpp:31-35, kept in registers).
-template <int NB>
-__device__ __forceinline__ void tally(uint32_t x, uint32_t top, uint32_t& above, uint32_t* bins) {
-  if (x >= top) ++above;
-  else if ((int)x >= (int)top - NB) atomicAdd(&bins[top - 1 - x], 1u);
-}
-
-// Suffix scan of one window (kernel.hpp:36-41): the smallest bin i whose
-// level x = top-1-i >= 1 has count(>= x) = C + sum(bins[0..i]) >= x.  Warp
-// version, lane l owns bins [8l, 8l+8).  Returns the level and, in `cnt`,
-// count(>= level).
-__device__ __forceinline__ bool warp_resolve(const uint32_t* bins, uint32_t C, uint32_t top,
-                                             uint32_t& level, uint32_t& cnt) {
-  static_assert(WARP_BINS == 256, "8 bins per lane");
-  const uint32_t lane = lane_id();
-  const uint4 b0 = reinterpret_cast<const uint4*>(bins)[2 * lane];
-  const uint4 b1 = reinterpret_cast<const uint4*>(bins)[2 * lane + 1];
-  const uint32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-  uint32_t s = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) s += b[j];
-  uint32_t run = C + warp_incl_scan(s) - s;
-  uint32_t found = 0xffffffffu, frun = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    run += b[j];
-    const int i = (int)lane * 8 + j;
-    const int x = (int)top - 1 - i;
-    if (found == 0xffffffffu && x >= 1 && run >= (uint32_t)x) {
-      found = (uint32_t)i;
-      frun = run;
-    }
-  }
-  const uint32_t g = __reduce_min_sync(FULL, found);
-  if (g == 0xffffffffu) return false;
-  cnt = __shfl_sync(FULL, frun, g >> 3);
-  level = top - 1 - g;
-  return true;
-}
-
-__device__ __forceinline__ void warp_zero_bins(uint32_t* bins) {
-  const uint32_t lane = lane_id();
-  reinterpret_cast<uint4*>(bins)[2 * lane] = make_uint4(0, 0, 0, 0);
-  reinterpret_cast<uint4*>(bins)[2 * lane + 1] = make_uint4(0, 0, 0, 0);
-  __syncwarp();
-}
-
-// ------------------------------------------------------------------------
-// Streaming over a row with 128-bit id loads: each of NT cooperating threads
-// takes 8 entries per step (two 16-byte loads, software-pipelined one step
-// ahead), gathers their 8 estimates, then hands (valid mask, ids, estimates)
-// to the callback.  Rows need not be 16-byte aligned: positions outside
-// [ob, oe) are masked (the adjacency has ADJ_PAD spare entries).
-// ------------------------------------------------------------------------
-template <int NT, typename OffT, typename EstT, typename F>
-__device__ __forceinline__ void stream_row(const P<OffT, EstT>& p, const EstT* snap, uint32_t me,
-                                           uint64_t ob, uint64_t oe, const EstT* s_cache,
-                                           uint32_t cache_n, F&& f) {
-  constexpr uint64_t STEP = (uint64_t)NT * 8;
-  uint64_t a = ob & ~(uint64_t)3;
-  uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-  if (a + 4 * me < oe) q0 = ld_ids4(p.adj, a + 4 * me);
-  if (a + 4 * me + 4 * NT < oe) q1 = ld_ids4(p.adj, a + 4 * me + 4 * NT);
-  for (; a < oe; a += STEP) {
-    uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
-    const uint64_t nb = a + STEP;
-    if (nb + 4 * me < oe) n0 = ld_ids4(p.adj, nb + 4 * me);
-    if (nb + 4 * me + 4 * NT < oe) n1 = ld_ids4(p.adj, nb + 4 * me + 4 * NT);
-    uint32_t ids[8], x[8];
-    uint32_t ok = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint64_t pos = a + 4 * me + (k >> 2) * 4 * NT + (k & 3);
-      ids[k] = u4_get(k < 4 ? q0 : q1, k & 3);
-      const bool v = pos >= ob && pos < oe;
-      ok |= (uint32_t)v << k;
-      x[k] = v ? est_at(s_cache, cache_n, snap, ids[k]) : 0u;
-    }
-    f(ok, ids, x);
-    q0 = n0;
-    q1 = n1;
-  }
-}
 
 // One evaluation result (the evaluate phase): lower N[u], keep cnt[u] exact.
 template <typename OffT, typename EstT>
@@ -446,18 +226,19 @@ __device__ __forceinline__ uint32_t grab_huge(const P<OffT, EstT>& p, const Roun
 template <typename OffT, typename EstT>
 __device__ __noinline__ void huge_window(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
                                          const EstT* s_cache, uint32_t* s_hist, uint32_t* s_red,
-                                         uint64_t ob, uint64_t oe, uint32_t cap, uint32_t* out) {
+                                         uint64_t ob, uint64_t oe, uint32_t cap, uint32_t lo,
+                                         uint32_t* out) {
   const uint32_t tid = threadIdx.x;
   uint32_t top = cap;
   for (;;) {
     for (int i = tid; i < HIST_BINS; i += SOLVE_THREADS) s_hist[i] = 0;
     __syncthreads();
     uint32_t above = 0;
-    stream_row<SOLVE_THREADS>(p, rv.snap, tid, ob, oe, s_cache, rv.cache_n,
+    stream_row<SOLVE_THREADS, true>(p.adj, rv.snap, tid, ob, oe, s_cache, rv.cache_n,
                               [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
                                 for (int k = 0; k < 8; ++k)
-                                  if (ok >> k & 1) tally<HIST_BINS>(x[k], top, above, s_hist);
+                                  if (ok >> k & 1) tally<HIST_BINS>(x[k], top, lo, above, s_hist);
                               });
     const uint32_t C = block_sum(above, s_red);
     constexpr int PER = HIST_BINS / SOLVE_THREADS;
@@ -515,7 +296,7 @@ __device__ void eval_huge(const P<OffT, EstT>& p, const RoundView<EstT>& rv, con
     uint32_t cA = 0;
     if (!rv.skip_a) {
       uint32_t c = 0;
-      stream_row<SOLVE_THREADS>(p, rv.snap, tid, ob, oe, s_cache, rv.cache_n,
+      stream_row<SOLVE_THREADS, true>(p.adj, rv.snap, tid, ob, oe, s_cache, rv.cache_n,
                                 [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
                                   for (int k = 0; k < 8; ++k) c += (ok >> k & 1) && x[k] >= cap;
@@ -525,7 +306,9 @@ __device__ void eval_huge(const P<OffT, EstT>& p, const RoundView<EstT>& rv, con
     }
     uint32_t t = cap, cn = cA;
     if (!keep) {
-      huge_window(p, rv, s_cache, s_hist, s_red, ob, oe, cap, s_out);
+      // counting rule: the new level is >= cnt[u] = count(>= cap)
+      const uint32_t lo = rv.skip_a ? p.cnt[u] : 0u;
+      huge_window(p, rv, s_cache, s_hist, s_red, ob, oe, cap, lo, s_out);
       t = s_out[0];
       cn = s_out[1];
     }
@@ -572,17 +355,17 @@ __device__ __forceinline__ Meta shfl_meta(const Meta& m, int src) {
 template <typename OffT, typename EstT>
 __device__ __noinline__ uint2 warp_window(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
                                           const EstT* s_cache, uint32_t* bins, uint64_t ob,
-                                          uint64_t oe, uint32_t cap) {
+                                          uint64_t oe, uint32_t cap, uint32_t lo) {
   const uint32_t lane = lane_id();
   uint32_t top = cap;
   for (;;) {
     warp_zero_bins(bins);
     uint32_t above = 0;
-    stream_row<32>(p, rv.snap, lane, ob, oe, s_cache, rv.cache_n,
+    stream_row<32, true>(p.adj, rv.snap, lane, ob, oe, s_cache, rv.cache_n,
                    [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
                      for (int k = 0; k < 8; ++k)
-                       if (ok >> k & 1) tally<WARP_BINS>(x[k], top, above, bins);
+                       if (ok >> k & 1) tally<WARP_BINS>(x[k], top, lo, above, bins);
                    });
     __syncwarp();
     const uint32_t C = __reduce_add_sync(FULL, above);
@@ -611,7 +394,7 @@ __device__ void eval_wstream(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
       uint32_t cA = 0;
       if (!rv.skip_a) {
         uint32_t c = 0;
-        stream_row<32>(p, rv.snap, lane, it.ob, it.oe, s_cache, rv.cache_n,
+        stream_row<32, true>(p.adj, rv.snap, lane, it.ob, it.oe, s_cache, rv.cache_n,
                        [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
                          for (int k = 0; k < 8; ++k) c += (ok >> k & 1) && x[k] >= cap;
@@ -620,7 +403,8 @@ __device__ void eval_wstream(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
         keep = cA >= cap;
       }
       uint2 tc = make_uint2(cap, cA);
-      if (!keep) tc = warp_window(p, rv, s_cache, bins, it.ob, it.oe, cap);
+      if (!keep)
+        tc = warp_window(p, rv, s_cache, bins, it.ob, it.oe, cap, rv.skip_a ? p.cnt[it.u] : 0u);
       if (lane == 0) finish_eval(p, rv, it.u, tc.x, cap, tc.y, it.oe - it.ob, acc);
     }
   });
@@ -630,13 +414,6 @@ __device__ void eval_wstream(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
 // SUB class (DEG_THREAD_MAX < deg <= DEG_SUB_MAX): 8-lane tile per vertex
 // (4 vertices per warp), 8 values per lane in registers, bisection.
 // ------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t tile8_sum(uint32_t v) {
-  v += __shfl_xor_sync(FULL, v, 4, 8);
-  v += __shfl_xor_sync(FULL, v, 2, 8);
-  v += __shfl_xor_sync(FULL, v, 1, 8);
-  return v;
-}
-
 template <typename OffT, typename EstT>
 __device__ void eval_sub(const P<OffT, EstT>& p, const RoundView<EstT>& rv, const EstT* s_cache,
                          Acc& acc) {
@@ -738,7 +515,7 @@ __device__ void notify_huge(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
     if (t < cap) {
       const uint64_t ob = p.off[u], oe = p.off[u + 1];
       if (tid == 0) acc.nscan += oe - ob;
-      stream_row<SOLVE_THREADS>(p, p.N, tid, ob, oe, s_cache, rv.cache_n,
+      stream_row<SOLVE_THREADS, true>(p.adj, p.N, tid, ob, oe, s_cache, rv.cache_n,
                                 [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
                                   notify_batch<8>(p, rv, ok, ids, x, t, cap, acc);
                                 });
@@ -761,7 +538,7 @@ __device__ void notify_wstream(const P<OffT, EstT>& p, const RoundView<EstT>& rv
       const uint32_t t = __shfl_sync(FULL, tn, i);
       if (t >= it.cap) continue;  // evaluated but did not drop (warp-uniform)
       if (lane == 0) acc.nscan += it.oe - it.ob;
-      stream_row<32>(p, (const EstT*)p.N, lane, it.ob, it.oe, s_cache, rv.cache_n,
+      stream_row<32, true>(p.adj, (const EstT*)p.N, lane, it.ob, it.oe, s_cache, rv.cache_n,
                      [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
                        notify_batch<8>(p, rv, ok, ids, x, t, it.cap, acc);
                      });
@@ -820,36 +597,18 @@ __device__ __forceinline__ void flush_acc(const P<OffT, EstT>& p, uint32_t sr, c
   }
 }
 
-template <typename EstT>
-__device__ __forceinline__ void fill_cache(EstT* s_cache, const EstT* src, uint32_t cache_n) {
-  // cache_n * sizeof(EstT) is a multiple of 16 bytes; 8 loads in flight per
-  // thread so the fill costs ~2 memory round trips, not nvec / SOLVE_THREADS
-  const uint4* s = reinterpret_cast<const uint4*>(src);
-  uint4* d = reinterpret_cast<uint4*>(s_cache);
-  const uint32_t nvec = (uint32_t)((size_t)cache_n * sizeof(EstT) / 16);
-  for (uint32_t i0 = threadIdx.x; i0 < nvec; i0 += 8 * SOLVE_THREADS) {
-    uint4 v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t i = i0 + k * SOLVE_THREADS;
-      if (i < nvec) v[k] = s[i];
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t i = i0 + k * SOLVE_THREADS;
-      if (i < nvec) d[i] = v[k];
-    }
-  }
-}
-
+#ifndef KC_CTAS_PER_SM
+#define KC_CTAS_PER_SM 1
+#endif
 template <typename OffT, typename EstT>
-__global__ void __launch_bounds__(SOLVE_THREADS, 1) rounds_kernel(P<OffT, EstT> p) {
+__global__ void __launch_bounds__(SOLVE_THREADS, KC_CTAS_PER_SM) rounds_kernel(P<OffT, EstT> p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem[];
   EstT* s_cache = reinterpret_cast<EstT*>(smem);
   const size_t cache_bytes = ((size_t)p.cache_n * sizeof(EstT) + 15) & ~(size_t)15;
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(smem + cache_bytes);
-  // per-warp histogram bins (alias s_hist once the HUGE phase is over)
+  // per-warp regions (alias s_hist once the HUGE phase is over):
+  // windowed-histogram bins + the flat-stream batch state
   uint32_t* w_bins = s_hist + WARP_BINS * warp_id();
   __shared__ uint32_t s_red[33];
   __shared__ uint32_t s_item;
@@ -890,6 +649,11 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) rounds_kernel(P<OffT, EstT> 
 #pragma unroll
     for (int c = 0; c < NCLS; ++c) active += rv.qcnt[c];
     const uint32_t cache_n = active >= CACHE_MIN_ACTIVE ? p.cache_n : 0u;
+    if (blockIdx.x == 0 && tid == 0) {
+      p.stats[sr].q01 = rv.qcnt[0] | (unsigned long long)rv.qcnt[1] << 32;
+      p.stats[sr].q23 = rv.qcnt[2] | (unsigned long long)rv.qcnt[3] << 32;
+      p.stats[sr].q4 = rv.qcnt[4];
+    }
     rv.cache_n = cache_n;
     if (cache_n) fill_cache(s_cache, (const EstT*)p.E, cache_n);
     __syncthreads();
@@ -898,11 +662,13 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) rounds_kernel(P<OffT, EstT> 
     // ---------------- EVALUATE ----------------
     eval_huge(p, rv, s_cache, s_hist, s_red, &s_item, acc);
     if (pf) pf[2] = gtimer();
-    eval_wstream<G_BIG>(p, rv, s_cache, C_BIG, w_bins, acc);
-    eval_wstream<G_WARP>(p, rv, s_cache, C_WARP, w_bins, acc);
-    if (pf) pf[3] = gtimer();
-    eval_sub(p, rv, s_cache, acc);
-    eval_thread(p, rv, s_cache, acc);
+    {
+      eval_wstream<G_BIG>(p, rv, s_cache, C_BIG, w_bins, acc);
+      eval_wstream<G_WARP>(p, rv, s_cache, C_WARP, w_bins, acc);
+      if (pf) pf[3] = gtimer();
+      eval_sub(p, rv, s_cache, acc);
+      eval_thread(p, rv, s_cache, acc);
+    }
     if (pf) pf[4] = gtimer();
     if (__any_sync(FULL, acc.any_drop) && lane_id() == 0) s_drop = 1;
     __syncthreads();
@@ -931,10 +697,12 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) rounds_kernel(P<OffT, EstT> 
     __syncthreads();
     if (pf) pf[6] = gtimer();
     notify_huge(p, rv, s_cache, &s_item, acc);
-    notify_wstream<G_BIG>(p, rv, s_cache, C_BIG, acc);
-    notify_wstream<G_WARP>(p, rv, s_cache, C_WARP, acc);
-    notify_small<G_SUB>(p, rv, s_cache, C_SUB, acc);
-    notify_small<G_THREAD>(p, rv, s_cache, C_THREAD, acc);
+    {
+      notify_wstream<G_BIG>(p, rv, s_cache, C_BIG, acc);
+      notify_wstream<G_WARP>(p, rv, s_cache, C_WARP, acc);
+      notify_small<G_SUB>(p, rv, s_cache, C_SUB, acc);
+      notify_small<G_THREAD>(p, rv, s_cache, C_THREAD, acc);
+    }
     flush_acc(p, sr, acc, s_acc);
     grid.sync();
     if (pf) pf[7] = gtimer();
@@ -1015,7 +783,8 @@ cudaError_t launch_rounds_t(const SolveBuffers& b, const SolveConfig& c, uint32_
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SOLVE_THREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  dim3 grid(c.num_sms), block(SOLVE_THREADS);
+  const int ctas = per_sm < KC_CTAS_PER_SM ? per_sm : KC_CTAS_PER_SM;
+  dim3 grid(c.num_sms * ctas), block(SOLVE_THREADS);
   void* args[] = {&p};
   return cudaLaunchCooperativeKernel((const void*)kern, grid, block, args, smem, stream);
 }

@@ -24,12 +24,18 @@ core, st = g.solve(o)
 print("instrumented solve ms", st["t_solve_ms"])
 pt = g.phase_times().astype(np.int64)
 R = min(st["iterations"], 256)
-names = ["cache", "huge", "big", "warp", "sub", "thread", "sync+apply"]
+names = ["compact", "ev_huge", "ev_bigwarp", "ev_small", "sync1", "fillN", "notify+s2"]
+rs = g.round_stats(R).astype(np.int64)
 t0 = pt[0, :, 0].min()
-print("round  start_us  " + " ".join(f"{n:>10s}" for n in names) + "   (max over CTAs, us)")
+print("round  start_us  " + " ".join(f"{n:>10s}" for n in names) +
+      "   |  evals   escan(M) ascan(M) nscan(M) fires(M)  q:huge big warp sub thread  (max over CTAs, us)")
 tot = np.zeros(7)
 for r in range(R):
     d = np.diff(pt[r], axis=1) / 1e3  # per CTA per phase
     mx = d.max(axis=0); tot += mx
-    print(f"{r:5d} {(pt[r,:,0].min()-t0)/1e3:9.1f}  " + " ".join(f"{x:10.1f}" for x in mx))
+    q = rs[r]
+    qs = [q[6] & 0xffffffff, q[6] >> 32, q[7] & 0xffffffff, q[7] >> 32, q[8]]
+    print(f"{r:5d} {(pt[r,:,0].min()-t0)/1e3:9.1f}  " + " ".join(f"{x:10.1f}" for x in mx) +
+          f"   | {q[0]:8d} {q[1]/1e6:8.2f} {q[5]/1e6:8.2f} {q[4]/1e6:8.2f} {q[3]/1e6:8.2f}  " + " ".join(str(int(v)) for v in qs))
+print("totals: escan %.1fM ascan %.1fM nscan %.1fM" % (rs[:,1].sum()/1e6, rs[:,5].sum()/1e6, rs[:,4].sum()/1e6))
 print("sum of max:", " ".join(f"{n}={x:.0f}" for n, x in zip(names, tot)))

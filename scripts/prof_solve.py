@@ -12,11 +12,15 @@ ap.add_argument("--scale", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--rule", type=int, default=2)
 ap.add_argument("--cache", type=int, default=0)
+ap.add_argument("--legacy", action="store_true", help="counting rule on the flag-frontier solver")
 a = ap.parse_args()
 desc, (p0, p1, p2), seed = CONFIGS[a.config]
 if a.scale: p0 = a.scale
 d = K.gen_config(a.config, p0, p1, p2, seed=seed)
 g = K.GpuGraph(d)
 for i in range(a.reps):
-    core, st = g.solve(K.FastKOptions(rule=K.Rule(a.rule), smem_cache=a.cache))
+    o = K.FastKOptions(rule=K.Rule(a.rule), smem_cache=a.cache)
+    if a.legacy:
+        o.debug_flags = K.api.KC_DEBUG_LEGACY_COUNT
+    core, st = g.solve(o)
     print(i, {k: st[k] for k in ("iterations", "e_scan", "v_eval", "t_solve_ms", "k_max")}, flush=True)
