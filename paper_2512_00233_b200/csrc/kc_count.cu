@@ -61,7 +61,11 @@ constexpr uint32_t CACHE_MIN_ACTIVE = 4096;  // smaller rounds skip the shared-m
 #endif
 constexpr uint32_t LIST_MIN_DEG = KC_LIST_MIN_DEG;  // rows longer than this keep a list
 constexpr uint32_t WARP_MAX_LEN = DEG_BIG_MAX;  // longest scan a single warp takes
+constexpr int HREG = HIST_BINS > (int)NWARPS * WARP_BINS ? HIST_BINS : (int)NWARPS * WARP_BINS;
 constexpr int WQ = 64;             // per-warp, per-class enqueue buffer (flushed at 32)
+#ifndef KC_R0_PASSA
+#define KC_R0_PASSA 0              // 1: round 0 first counts values >= cap (one pass when
+#endif                             //    nothing drops); 0: straight to the window
 #ifndef KC_LIST_COMPACT
 #define KC_LIST_COMPACT 0          // 1: notify filters lists in place (warp scans)
 #endif
@@ -159,43 +163,40 @@ __device__ __forceinline__ void for_class(const CP<OffT, EstT>& p, const View<Es
 // ids[k]) go to the warp's shared buffer of their class; a buffer holding
 // >= 32 ids is flushed with one global atomicAdd.
 // ------------------------------------------------------------------------
+struct Enq {            // the warp's view of the next round's queue
+  uint32_t* qn;         // next round's class sizes
+  uint32_t* qnext;      // next round's queue
+  uint32_t* wbuf;       // this warp's buffers [NCLS][WQ] (shared memory)
+  uint32_t* wn;         // this warp's buffer fill levels [NCLS] (shared memory)
+};
+
 template <typename OffT, typename EstT>
-__device__ __noinline__ void wq_flush(const CP<OffT, EstT>& p, const View<EstT>& v, uint32_t* wbuf,
-                                      uint32_t* wn, int c) {
-  const uint32_t n = wn[c];
+__device__ __noinline__ void wq_flush(const CP<OffT, EstT>& p, const Enq& q, int c) {
+  const uint32_t n = q.wn[c];
   if (n == 0) return;
   uint32_t base = 0;
-  if (lane_id() == 0) base = atomicAdd(&v.qn[c], n);
+  if (lane_id() == 0) base = atomicAdd(&q.qn[c], n);
   base = __shfl_sync(FULL, base, 0);
-  for (uint32_t i = lane_id(); i < n; i += 32) v.qnext[p.cb[c] + base + i] = wbuf[c * WQ + i];
+  for (uint32_t i = lane_id(); i < n; i += 32) q.qnext[p.cb[c] + base + i] = q.wbuf[c * WQ + i];
   __syncwarp();
-  if (lane_id() == 0) wn[c] = 0;
+  if (lane_id() == 0) q.wn[c] = 0;
   __syncwarp();
 }
 
+// One activation per lane at most (a: this lane activates `id`).
 template <typename OffT, typename EstT>
-__device__ __noinline__ void wq_push(const CP<OffT, EstT>& p, const View<EstT>& v, uint32_t* wbuf,
-                                     uint32_t* wn, uint32_t act, const uint32_t (&ids)[8]) {
+__device__ __noinline__ void wq_push(const CP<OffT, EstT>& p, const Enq& q, bool a, uint32_t id) {
+  const int c = a ? cls_of(p, id) : NCLS;
 #pragma unroll 1
-  for (int k = 0; k < 8; ++k) {
-    const bool a = act >> k & 1;
-    if (!__any_sync(FULL, a)) continue;
-    uint32_t id = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j == k) id = ids[j];
-    const int c = a ? cls_of(p, id) : NCLS;
-#pragma unroll 1
-    for (int cc = 0; cc < NCLS; ++cc) {
-      const uint32_t m = __ballot_sync(FULL, c == cc);
-      if (!m) continue;
-      const uint32_t n0 = wn[cc];
-      if (c == cc) wbuf[cc * WQ + n0 + __popc(m & lanemask_lt())] = id;
-      __syncwarp();
-      if (lane_id() == 0) wn[cc] = n0 + __popc(m);
-      __syncwarp();
-      if (n0 + __popc(m) >= 32) wq_flush(p, v, wbuf, wn, cc);
-    }
+  for (int cc = 0; cc < NCLS; ++cc) {
+    const uint32_t m = __ballot_sync(FULL, c == cc);
+    if (!m) continue;
+    const uint32_t n0 = q.wn[cc];
+    if (c == cc) q.wbuf[cc * WQ + n0 + __popc(m & lanemask_lt())] = id;
+    __syncwarp();
+    if (lane_id() == 0) q.wn[cc] = n0 + __popc(m);
+    __syncwarp();
+    if (n0 + __popc(m) >= 32) wq_flush(p, q, cc);
   }
 }
 
@@ -203,24 +204,28 @@ __device__ __noinline__ void wq_push(const CP<OffT, EstT>& p, const View<EstT>& 
 // x[k] (valid where bit k of ok): decrement cnt[w] where should_notify(t,
 // cap, N[w]) holds (fastk.hpp:25-27); the decrement that takes cnt[w] below
 // N[w] activates w.  All atomics are issued before any result is consumed.
+// Warp-converged.
 template <typename OffT, typename EstT>
-__device__ __forceinline__ void notify8(const CP<OffT, EstT>& p, const View<EstT>& v,
-                                        uint32_t* wbuf, uint32_t* wn, uint32_t ok,
+__device__ __forceinline__ void notify8(const CP<OffT, EstT>& p, const Enq& q, uint32_t ok,
                                         const uint32_t (&ids)[8], const uint32_t (&x)[8],
-                                        uint32_t t, uint32_t cap, Acc& acc) {
+                                        uint32_t t, uint32_t cap, uint32_t& fires) {
   uint32_t fire = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) fire |= (uint32_t)((ok >> k & 1) && t < x[k] && x[k] <= cap) << k;
   uint32_t act = 0;
   if (fire) {
-    acc.fires += __popc(fire);
+    fires += __popc(fire);
     uint32_t old[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) old[k] = (fire >> k & 1) ? atomicSub(&p.cnt[ids[k]], 1u) : 0u;
 #pragma unroll
     for (int k = 0; k < 8; ++k) act |= (uint32_t)((fire >> k & 1) && old[k] == x[k]) << k;
   }
-  if (__any_sync(FULL, act)) wq_push(p, v, wbuf, wn, act, ids);
+  if (__any_sync(FULL, act)) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (__any_sync(FULL, act >> k & 1)) wq_push(p, q, (act >> k & 1) != 0, ids[k]);
+  }
 }
 
 // ------------------------------------------------------------------------
@@ -245,6 +250,7 @@ __device__ __noinline__ uint2 warp_window(const uint32_t* src, const EstT* snap,
                        });
     __syncwarp();
     const uint32_t C = __reduce_add_sync(FULL, above);
+    if (top == cap && C >= cap) return make_uint2(cap, C);  // no drop (round 0 only)
     uint32_t level = 0, c = 0;
     const bool hit = warp_resolve(bins, C, top, level, c, lo > 1u ? lo : 1u);
     __syncwarp();
@@ -272,12 +278,20 @@ __device__ __noinline__ void cta_window(const uint32_t* src, const EstT* snap, c
                                       if (ok >> k & 1) tally<HIST_BINS>(x[k], top, lo, above, s_hist);
                                   });
     const uint32_t C = block_sum(above, s_red);
-    constexpr int PER = HIST_BINS / SOLVE_THREADS;
+    if (top == cap && C >= cap) {  // no drop (round 0 only)
+      if (tid == 0) {
+        out[0] = cap;
+        out[1] = C;
+      }
+      __syncthreads();
+      return;
+    }
+    constexpr int PER = (HIST_BINS + SOLVE_THREADS - 1) / SOLVE_THREADS;  // bins per thread
     uint32_t h[PER];
     uint32_t sm = 0;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-      h[j] = s_hist[tid * PER + j];
+      h[j] = tid * PER + j < HIST_BINS ? s_hist[tid * PER + j] : 0u;
       sm += h[j];
     }
     uint32_t run = C + block_excl_scan(sm, s_red);
@@ -287,7 +301,7 @@ __device__ __noinline__ void cta_window(const uint32_t* src, const EstT* snap, c
     for (int j = 0; j < PER; ++j) {
       run += h[j];
       const int i = tid * PER + j;
-      const int x = (int)top - 1 - i;
+      const int x = i < HIST_BINS ? (int)top - 1 - i : 0;  // x = 0 never qualifies
       if (found == 0xffffffffu && x >= (int)minlvl && run >= (uint32_t)x) {
         found = (uint32_t)i;
         frun = run;
@@ -374,12 +388,12 @@ __device__ __forceinline__ void finish_eval(const CP<OffT, EstT>& p, const Item&
 }
 
 template <typename OffT, typename EstT>
-__device__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+__device__ __noinline__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                           uint32_t* bins, const Item& it, Acc& acc) {
   const EstT* snap = v.snap;
   const uint32_t cache_n = v.cache_n;
   uint32_t lo = it.lo;
-  if (v.r0) {
+  if (KC_R0_PASSA && v.r0) {
     const uint32_t cA = warp_count_ge(p.adj, snap, s_cache, cache_n, it.ob, it.ob + it.deg, it.cap);
     if (cA >= it.cap) {
       if (lane_id() == 0) finish_eval(p, it, it.cap, cA, it.deg, acc);
@@ -403,13 +417,13 @@ __device__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>& v, const Es
 }
 
 template <typename OffT, typename EstT>
-__device__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+__device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                          uint32_t* s_hist, Shared& sh, uint32_t u, Acc& acc) {
   const Item it = eval_item(p, v, s_cache, u);
   const EstT* snap = v.snap;
   const uint32_t cache_n = v.cache_n;
   uint32_t lo = it.lo;
-  if (v.r0) {
+  if (KC_R0_PASSA && v.r0) {
     uint32_t c = 0;
     stream_row<SOLVE_THREADS, true>(p.adj, snap, threadIdx.x, it.ob, it.ob + it.deg, s_cache,
                                     cache_n,
@@ -651,17 +665,19 @@ __device__ __forceinline__ uint32_t list_threshold(uint32_t t) {
   return L ? L : 1u;
 }
 
+// Returns the notifications fired by this lane (counted once per warp in
+// `acc` by the callers).
 template <bool RO, typename OffT, typename EstT>
-__device__ __noinline__ void notify_warp(const CP<OffT, EstT>& p, const View<EstT>& v,
-                                         const EstT* s_cache, uint32_t* wbuf, uint32_t* wn,
-                                         const uint32_t* src, uint32_t u, uint64_t ob,
-                                         uint32_t len, uint32_t t, uint32_t cap, uint32_t build,
-                                         Acc& acc) {
+__device__ __noinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const Enq& q,
+                                             const EstT* s_cache, uint32_t cache_n,
+                                             const uint32_t* src, uint32_t u, uint64_t ob,
+                                             uint32_t len, uint32_t t, uint32_t cap,
+                                             uint32_t build) {
   uint32_t cursor = 0;  // warp-uniform
-  const uint32_t cache_n = v.cache_n;
+  uint32_t fires = 0;
   stream_row<32, RO>(src, p.N, lane_id(), ob, ob + len, s_cache, cache_n,
                      [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
-                       notify8(p, v, wbuf, wn, ok, ids, x, t, cap, acc);
+                       notify8(p, q, ok, ids, x, t, cap, fires);
                        if (build) {
                          uint32_t keep = 0;
 #pragma unroll
@@ -676,27 +692,27 @@ __device__ __noinline__ void notify_warp(const CP<OffT, EstT>& p, const View<Est
                        }
                      });
   if (lane_id() == 0) {
-    acc.nscan += len;
     if (build) {
       p.rlen[u] = cursor;
       p.rthr[u] = (EstT)build;
     }
     p.E[u] = (EstT)t;  // apply (fastk.cpp:153)
   }
+  return fires;
 }
 
 template <bool RO, typename OffT, typename EstT>
-__device__ __noinline__ void notify_cta(const CP<OffT, EstT>& p, const View<EstT>& v,
-                                        const EstT* s_cache, uint32_t* wbuf, uint32_t* wn,
-                                        Shared& sh, const uint32_t* src, uint32_t u, uint64_t ob,
-                                        uint32_t len, uint32_t t, uint32_t cap, uint32_t build,
-                                        Acc& acc) {
+__device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p, const Enq& q,
+                                            const EstT* s_cache, uint32_t cache_n, Shared& sh,
+                                            const uint32_t* src, uint32_t u, uint64_t ob,
+                                            uint32_t len, uint32_t t, uint32_t cap,
+                                            uint32_t build) {
   if (threadIdx.x == 0) sh.cursor = 0;
   __syncthreads();
-  const uint32_t cache_n = v.cache_n;
+  uint32_t fires = 0;
   stream_row<SOLVE_THREADS, RO>(src, p.N, threadIdx.x, ob, ob + len, s_cache, cache_n,
                                 [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
-                                  notify8(p, v, wbuf, wn, ok, ids, x, t, cap, acc);
+                                  notify8(p, q, ok, ids, x, t, cap, fires);
                                   if (build) {
                                     uint32_t keep = 0;
 #pragma unroll
@@ -715,7 +731,6 @@ __device__ __noinline__ void notify_cta(const CP<OffT, EstT>& p, const View<EstT
                                 });
   __syncthreads();
   if (threadIdx.x == 0) {
-    acc.nscan += len;
     if (build) {
       p.rlen[u] = sh.cursor;
       p.rthr[u] = (EstT)build;
@@ -723,6 +738,7 @@ __device__ __noinline__ void notify_cta(const CP<OffT, EstT>& p, const View<EstT
     p.E[u] = (EstT)t;
   }
   __syncthreads();
+  return fires;
 }
 
 struct Drop {
@@ -747,21 +763,29 @@ __device__ __forceinline__ Drop drop_item(const CP<OffT, EstT>& p, uint32_t u) {
   return d;
 }
 
-template <typename OffT, typename EstT>
-__device__ __forceinline__ void notify_drop_warp(const CP<OffT, EstT>& p, const View<EstT>& v,
-                                                 const EstT* s_cache, uint32_t* wbuf, uint32_t* wn,
-                                                 const Drop& d, Acc& acc) {
-  if (d.thr)  // in place: drop entries whose settled value fell below the threshold
-    notify_warp<false>(p, v, s_cache, wbuf, wn, p.radj, d.u, d.ob, d.len, d.t, d.cap,
-                       KC_LIST_COMPACT ? d.thr : 0u, acc);
-  else
-    notify_warp<true>(p, v, s_cache, wbuf, wn, p.adj, d.u, d.ob, d.len, d.t, d.cap,
-                      (!v.r0 && d.deg > LIST_MIN_DEG) ? list_threshold(d.t) : 0u, acc);
+__device__ __forceinline__ uint32_t list_build(bool r0, const Drop& d) {
+  return (!r0 && d.deg > LIST_MIN_DEG) ? list_threshold(d.t) : 0u;
 }
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
-                              uint32_t* wbuf, uint32_t* wn, int c, uint32_t gmax, Acc& acc) {
+__device__ __forceinline__ uint32_t notify_drop_warp(const CP<OffT, EstT>& p, const Enq& q,
+                                                     const EstT* s_cache, uint32_t cache_n,
+                                                     bool r0, const Drop& d) {
+  if (d.thr)  // optionally in place: drop entries whose settled value fell below the threshold
+    return notify_warp<false>(p, q, s_cache, cache_n, p.radj, d.u, d.ob, d.len, d.t, d.cap,
+                              KC_LIST_COMPACT ? d.thr : 0u);
+  return notify_warp<true>(p, q, s_cache, cache_n, p.adj, d.u, d.ob, d.len, d.t, d.cap,
+                           list_build(r0, d));
+}
+
+template <typename OffT, typename EstT>
+__device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                           const Enq& q, const EstT* s_cache, int c,
+                                           uint32_t gmax, Acc& acc) {
+  const uint32_t cache_n = v.cache_n;
+  const bool r0 = v.r0;
+  uint32_t fires = 0;
+  unsigned long long nscan = 0;
   for_class(p, v, c, gmax, [&](uint32_t u, uint32_t n) {
     Drop mine{};
     if (lane_id() < n) mine = drop_item(p, u);
@@ -775,17 +799,21 @@ __device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p, const View<E
       d.len = __shfl_sync(FULL, mine.len, i);
       d.deg = __shfl_sync(FULL, mine.deg, i);
       d.ob = __shfl_sync(FULL, mine.ob, i);
-      notify_drop_warp(p, v, s_cache, wbuf, wn, d, acc);
+      fires += notify_drop_warp(p, q, s_cache, cache_n, r0, d);
+      nscan += d.len;
     }
   });
+  acc.fires += fires;
+  if (lane_id() == 0) acc.nscan += nscan;
 }
 
 // SUB and THREAD droppers: 8-lane tile per dropper, up to 8 neighbours per lane.
 template <typename OffT, typename EstT>
-__device__ __noinline__ void notify_small(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
-                             uint32_t* wbuf, uint32_t* wn, int c, Acc& acc) {
+__device__ __noinline__ void notify_small(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                          const Enq& q, const EstT* s_cache, int c, Acc& acc) {
   const uint32_t g = lane_id() >> 3, k = lane_id() & 7;
   const uint32_t cache_n = v.cache_n;
+  uint32_t fires = 0, nscan = 0;
   for_class(p, v, c, GMAX_SMALL, [&](uint32_t mu, uint32_t n) {
     for (uint32_t i0 = 0; i0 < n; i0 += 4) {
       const uint32_t u = __shfl_sync(FULL, mu, (int)(i0 + g) & 31);
@@ -809,13 +837,15 @@ __device__ __noinline__ void notify_small(const CP<OffT, EstT>& p, const View<Es
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         x[j] = (ok >> j & 1) ? est_at(s_cache, cache_n, (const EstT*)p.N, ids[j]) : 0u;
-      notify8(p, v, wbuf, wn, ok, ids, x, t, cap, acc);  // warp-converged
+      notify8(p, q, ok, ids, x, t, cap, fires);  // warp-converged
       if (k == 0 && t < cap) {
-        acc.nscan += deg;
+        nscan += deg;
         p.E[u] = (EstT)t;
       }
     }
   });
+  acc.fires += fires;
+  acc.nscan += nscan;
 }
 
 template <typename OffT, typename EstT>
@@ -840,19 +870,21 @@ __device__ __forceinline__ void flush_acc(const CP<OffT, EstT>& p, uint32_t sr, 
 }
 
 template <typename OffT, typename EstT>
-__global__ void __launch_bounds__(SOLVE_THREADS, 1) count_kernel(const __grid_constant__ CP<OffT, EstT> p) {
+__global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __grid_constant__ CP<OffT, EstT> p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem[];
   EstT* s_cache = reinterpret_cast<EstT*>(smem);
   const size_t cache_bytes = ((size_t)p.cache_n * sizeof(EstT) + 15) & ~(size_t)15;
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(smem + cache_bytes);  // CTA window / warp bins
   uint32_t* w_bins = s_hist + WARP_BINS * warp_id();
-  uint32_t* s_wq = s_hist + HIST_BINS;  // per-warp enqueue buffers
-  uint32_t* wbuf = s_wq + (size_t)warp_id() * NCLS * WQ;
+  uint32_t* s_wq = s_hist + HREG;  // per-warp enqueue buffers
   __shared__ uint32_t s_wn[NWARPS][NCLS];
   __shared__ Shared sh;
   uint32_t* wn = s_wn[warp_id()];
   const uint32_t tid = threadIdx.x;
+  Enq q;
+  q.wbuf = s_wq + (size_t)warp_id() * NCLS * WQ;
+  q.wn = wn;
   if (tid == 0) sh.ticket = 0xffffffffu;
   if (lane_id() < NCLS) wn[lane_id()] = 0;
   __syncthreads();
@@ -867,6 +899,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_kernel(const __grid_co
     v.grab = p.ctl[cur].grab;
     v.qn = p.ctl[nxt].qcnt;
     v.qnext = p.queue[nxt];
+    q.qn = v.qn;
+    q.qnext = v.qnext;
     v.r0 = r == 0;
     unsigned long long* pf = (p.prof && r < PROF_ROUNDS && tid == 0)
                                  ? p.prof + ((size_t)r * gridDim.x + blockIdx.x) * PROF_PHASES
@@ -951,12 +985,13 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_kernel(const __grid_co
     if (pf) pf[6] = gtimer();
     auto notify_long = [&](uint32_t u) {
       const Drop d = drop_item(p, u);  // a long-queued hub always dropped
-      if (d.thr)
-        notify_cta<false>(p, v, s_cache, wbuf, wn, sh, p.radj, d.u, d.ob, d.len, d.t, d.cap, 0u,
-                          acc);
-      else
-        notify_cta<true>(p, v, s_cache, wbuf, wn, sh, p.adj, d.u, d.ob, d.len, d.t, d.cap,
-                         v.r0 ? 0u : list_threshold(d.t), acc);
+      const uint32_t f =
+          d.thr ? notify_cta<false>(p, q, s_cache, cache_n, sh, p.radj, d.u, d.ob, d.len, d.t,
+                                    d.cap, 0u)
+                : notify_cta<true>(p, q, s_cache, cache_n, sh, p.adj, d.u, d.ob, d.len, d.t,
+                                   d.cap, list_build(v.r0, d));
+      acc.fires += f;
+      if (tid == 0) acc.nscan += d.len;
     };
     huge_warps(
         p, v, sh, ctl, 1,
@@ -966,16 +1001,19 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_kernel(const __grid_co
         },
         [&](uint32_t u) {
           const Drop d = drop_item(p, u);
-          if (d.t < d.cap) notify_drop_warp(p, v, s_cache, wbuf, wn, d, acc);
+          if (d.t < d.cap) {
+            acc.fires += notify_drop_warp(p, q, s_cache, cache_n, v.r0, d);
+            if (lane_id() == 0) acc.nscan += d.len;
+          }
         });
     consume_long(p, v, sh, ctl, 1, false, notify_long);
-    notify_wclass(p, v, s_cache, wbuf, wn, C_BIG, GMAX_BIG, acc);
-    notify_wclass(p, v, s_cache, wbuf, wn, C_WARP, GMAX_WARP, acc);
-    notify_small(p, v, s_cache, wbuf, wn, C_SUB, acc);
-    notify_small(p, v, s_cache, wbuf, wn, C_THREAD, acc);
+    notify_wclass(p, v, q, s_cache, C_BIG, GMAX_BIG, acc);
+    notify_wclass(p, v, q, s_cache, C_WARP, GMAX_WARP, acc);
+    notify_small(p, v, q, s_cache, C_SUB, acc);
+    notify_small(p, v, q, s_cache, C_THREAD, acc);
     consume_long(p, v, sh, ctl, 1, true, notify_long);
 #pragma unroll 1
-    for (int c = 0; c < NCLS; ++c) wq_flush(p, v, wbuf, wn, c);
+    for (int c = 0; c < NCLS; ++c) wq_flush(p, q, c);
     flush_acc(p, sr, acc, sh.acc);
     grid.sync();
     if (pf) pf[7] = gtimer();
@@ -1050,9 +1088,8 @@ cudaError_t launch_t(const SolveBuffers& b, const SolveConfig& c, uint32_t r_beg
   p.cache_n = c.cache_n;
   p.clamp_drop = c.clamp_drop;
   const size_t smem = (((size_t)c.cache_n * sizeof(EstT) + 15) & ~(size_t)15) +
-                      ((size_t)HIST_BINS + (size_t)NWARPS * NCLS * WQ) * sizeof(uint32_t);
-  static_assert(HIST_BINS >= (int)NWARPS * WARP_BINS, "warp bins alias the CTA histogram");
-  auto kern = count_kernel<OffT, EstT>;
+                      ((size_t)HREG + (size_t)NWARPS * NCLS * WQ) * sizeof(uint32_t);
+  auto kern = count_rounds_kernel<OffT, EstT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;

@@ -18,7 +18,7 @@ constexpr uint32_t DEG_WARP_MAX = 1020;  // WARP:   warp per vertex, 32 values p
 constexpr uint32_t DEG_BIG_MAX = 8192;   // BIG:    warp per vertex, streamed, warp histogram
                                          // HUGE:   CTA per vertex, streamed, CTA histogram
 #ifndef KC_SOLVE_THREADS
-#define KC_SOLVE_THREADS 512
+#define KC_SOLVE_THREADS 768
 #endif
 constexpr int SOLVE_THREADS = KC_SOLVE_THREADS;
 constexpr int HIST_BINS = 4096;          // CTA windowed histogram (16 KB of shared memory)

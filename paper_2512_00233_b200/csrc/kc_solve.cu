@@ -241,12 +241,12 @@ __device__ __noinline__ void huge_window(const P<OffT, EstT>& p, const RoundView
                                   if (ok >> k & 1) tally<HIST_BINS>(x[k], top, lo, above, s_hist);
                               });
     const uint32_t C = block_sum(above, s_red);
-    constexpr int PER = HIST_BINS / SOLVE_THREADS;
+    constexpr int PER = (HIST_BINS + SOLVE_THREADS - 1) / SOLVE_THREADS;  // bins per thread
     uint32_t h[PER];
     uint32_t sm = 0;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-      h[j] = s_hist[tid * PER + j];
+      h[j] = tid * PER + j < HIST_BINS ? s_hist[tid * PER + j] : 0u;
       sm += h[j];
     }
     uint32_t run = C + block_excl_scan(sm, s_red);
@@ -255,7 +255,7 @@ __device__ __noinline__ void huge_window(const P<OffT, EstT>& p, const RoundView
     for (int j = 0; j < PER; ++j) {
       run += h[j];
       const int i = tid * PER + j;
-      const int x = (int)top - 1 - i;
+      const int x = i < HIST_BINS ? (int)top - 1 - i : 0;  // x = 0 never qualifies
       if (found == 0xffffffffu && x >= 1 && run >= (uint32_t)x) {
         found = (uint32_t)i;
         frun = run;

@@ -1,12 +1,14 @@
 """Attribute ncu SASS-level stall samples to CUDA source lines.
 
-usage: python scripts/ncu_lines.py <report.ncu-rep> <kernel-substring> [topN]
-Needs the in-tree build (paper_2512_00233_b200/_build/kc_solve.o, -lineinfo).
+usage: python scripts/ncu_lines.py <report.ncu-rep> <kernel-substring> [topN] [object]
+Needs the in-tree build (paper_2512_00233_b200/_build/<object>.o, -lineinfo;
+object defaults to kc_count).
 """
 import collections, csv, io, os, re, subprocess, sys
 
 rep, kname = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+objname = sys.argv[4] if len(sys.argv) > 4 else "kc_count"
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
                      capture_output=True, text=True).stdout
@@ -17,10 +19,10 @@ si = hdr.index("Warp Stall Sampling (All Samples)")
 ie = hdr.index("Instructions Executed")
 stall_cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
 # SASS -> line map from the object file
-obj = os.path.join(root, "paper_2512_00233_b200", "_build", "kc_solve.o")
+obj = os.path.join(root, "paper_2512_00233_b200", "_build", objname + ".o")
 tmp = "/tmp/_kc_solve.cubin"
 subprocess.run(["cuobjdump", "-xelf", "all", obj], cwd="/tmp", capture_output=True)
-cub = [f for f in os.listdir("/tmp") if f.startswith("kc_solve") and f.endswith(".cubin")]
+cub = [f for f in os.listdir("/tmp") if f.startswith(objname) and f.endswith(".cubin")]
 dis = subprocess.run(["nvdisasm", "-g", os.path.join("/tmp", cub[0])], capture_output=True,
                      text=True).stdout
 fn = None
