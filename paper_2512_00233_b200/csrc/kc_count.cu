@@ -63,6 +63,12 @@ constexpr uint32_t LIST_MIN_DEG = KC_LIST_MIN_DEG;  // rows longer than this kee
 constexpr uint32_t WARP_MAX_LEN = DEG_BIG_MAX;  // longest scan a single warp takes
 constexpr int HREG = HIST_BINS > (int)NWARPS * WARP_BINS ? HIST_BINS : (int)NWARPS * WARP_BINS;
 constexpr int WQ = 64;             // per-warp, per-class enqueue buffer (flushed at 32)
+#ifndef KC_FLAT_EVAL
+#define KC_FLAT_EVAL 1             // rounds >= 1: batched flat streams for BIG / WARP evaluate
+#endif
+#ifndef KC_FLAT_NOTIFY
+#define KC_FLAT_NOTIFY 0           // ... and notify (slower: per-entry segment lookups)
+#endif
 #ifndef KC_R0_PASSA
 #define KC_R0_PASSA 0              // 1: round 0 first counts values >= cap (one pass when
 #endif                             //    nothing drops); 0: straight to the window
@@ -233,30 +239,61 @@ __device__ __forceinline__ void notify8(const CP<OffT, EstT>& p, const Enq& q, u
 // counted in registers, [top - NB, top) binned in shared memory, levels
 // below `lo` skipped (the answer is >= lo).  Returns (t, count(>= t)).
 // ------------------------------------------------------------------------
+// Windowed h-index over one row or list (kernel.hpp:31-41) for the levels
+// [max(lo, 1), cap]: values >= top are counted in registers, values in
+// [L, top) are binned in shared memory in coarse bins when the range is
+// wider than the bin count, then the qualifying bin is refined — at most two
+// passes for 16-bit estimates.  Values below lo are skipped (the answer is
+// known to be >= lo, or only levels >= lo are asked for).  Returns (t,
+// count(>= t)), (cap, count(>= cap)) when nothing drops, or (0, deg) when no
+// level >= lo qualifies.
 template <bool RO, typename EstT>
 __device__ __noinline__ uint2 warp_window(const uint32_t* src, const EstT* snap,
                                           const EstT* s_cache, uint32_t cache_n, uint32_t* bins,
                                           uint64_t ob, uint64_t oe, uint32_t cap, uint32_t lo,
-                                          uint32_t deg) {
+                                          uint32_t deg, bool fine_first) {
   uint32_t top = cap;
+  const uint32_t L0 = lo > 1u ? lo : 1u;
+  uint32_t L = L0;
+  bool fine = fine_first;
   for (;;) {
+    uint32_t range = top > L ? top - L : 0u;
+    if (fine && range > (uint32_t)WARP_BINS) {  // small drops first: one exact top window
+      L = top - WARP_BINS;
+      range = WARP_BINS;
+    }
+    fine = false;
+    const uint32_t w = range > (uint32_t)WARP_BINS ? (range + WARP_BINS - 1) / WARP_BINS : 1u;
     warp_zero_bins(bins);
     uint32_t above = 0;
     stream_row<32, RO>(src, snap, lane_id(), ob, oe, s_cache, cache_n,
                        [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
-                         for (int k = 0; k < 8; ++k)
-                           if (ok >> k & 1) tally<WARP_BINS>(x[k], top, lo, above, bins);
+                         for (int k = 0; k < 8; ++k) {
+                           if (!(ok >> k & 1)) continue;
+                           if (x[k] >= top) ++above;
+                           else if (x[k] >= L) atomicAdd(&bins[(top - 1 - x[k]) / w], 1u);
+                         }
                        });
     __syncwarp();
     const uint32_t C = __reduce_add_sync(FULL, above);
     if (top == cap && C >= cap) return make_uint2(cap, C);  // no drop (round 0 only)
-    uint32_t level = 0, c = 0;
-    const bool hit = warp_resolve(bins, C, top, level, c, lo > 1u ? lo : 1u);
+    uint32_t b = 0, run = 0;
+    const bool hit = range > 0 && warp_resolve_w(bins, C, top, w, L, b, run);
     __syncwarp();
-    if (hit) return make_uint2(level, c);
-    if ((int)top - WARP_BINS <= (int)lo) return make_uint2(0u, deg);  // only level 0 left
-    top -= WARP_BINS;
+    if (!hit) {
+      if (L > L0) {  // the top window missed: search the rest
+        top = L;
+        L = L0;
+        continue;
+      }
+      return make_uint2(0u, deg);
+    }
+    const uint32_t low = bin_low(top, w, L, b);
+    if (w == 1) return make_uint2(low, run);
+    // refine inside bin b: levels [low, top - b*w); level low qualifies
+    top -= b * w;
+    L = low;
   }
 }
 
@@ -264,18 +301,31 @@ template <bool RO, typename EstT>
 __device__ __noinline__ void cta_window(const uint32_t* src, const EstT* snap, const EstT* s_cache,
                                         uint32_t cache_n, uint32_t* s_hist, uint32_t* s_red,
                                         uint64_t ob, uint64_t oe, uint32_t cap, uint32_t lo,
-                                        uint32_t deg, uint32_t* out) {
+                                        uint32_t deg, bool fine_first, uint32_t* out) {
   const uint32_t tid = threadIdx.x;
   uint32_t top = cap;
+  const uint32_t L0 = lo > 1u ? lo : 1u;
+  uint32_t L = L0;
+  bool fine = fine_first;
   for (;;) {
+    uint32_t range = top > L ? top - L : 0u;
+    if (fine && range > (uint32_t)HIST_BINS) {  // small drops first: one exact top window
+      L = top - HIST_BINS;
+      range = HIST_BINS;
+    }
+    fine = false;
+    const uint32_t w = range > (uint32_t)HIST_BINS ? (range + HIST_BINS - 1) / HIST_BINS : 1u;
     for (int i = tid; i < HIST_BINS; i += SOLVE_THREADS) s_hist[i] = 0;
     __syncthreads();
     uint32_t above = 0;
     stream_row<SOLVE_THREADS, RO>(src, snap, tid, ob, oe, s_cache, cache_n,
                                   [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
-                                    for (int k = 0; k < 8; ++k)
-                                      if (ok >> k & 1) tally<HIST_BINS>(x[k], top, lo, above, s_hist);
+                                    for (int k = 0; k < 8; ++k) {
+                                      if (!(ok >> k & 1)) continue;
+                                      if (x[k] >= top) ++above;
+                                      else if (x[k] >= L) atomicAdd(&s_hist[(top - 1 - x[k]) / w], 1u);
+                                    }
                                   });
     const uint32_t C = block_sum(above, s_red);
     if (top == cap && C >= cap) {  // no drop (round 0 only)
@@ -295,28 +345,25 @@ __device__ __noinline__ void cta_window(const uint32_t* src, const EstT* snap, c
       sm += h[j];
     }
     uint32_t run = C + block_excl_scan(sm, s_red);
-    const uint32_t minlvl = lo > 1u ? lo : 1u;  // levels below the floor are incomplete
+    const uint32_t nb = range ? (range + w - 1) / w : 0u;
     uint32_t found = 0xffffffffu, frun = 0;
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       run += h[j];
-      const int i = tid * PER + j;
-      const int x = i < HIST_BINS ? (int)top - 1 - i : 0;  // x = 0 never qualifies
-      if (found == 0xffffffffu && x >= (int)minlvl && run >= (uint32_t)x) {
-        found = (uint32_t)i;
+      const uint32_t i = tid * PER + j;
+      if (found == 0xffffffffu && i < nb && run >= bin_low(top, w, L, i)) {
+        found = i;
         frun = run;
       }
     }
     const uint32_t g = block_min(found, s_red);
-    if (g != 0xffffffffu) {
-      if (found == g) {
-        out[0] = top - 1 - g;
-        out[1] = frun;
+    if (g == 0xffffffffu) {
+      if (L > L0) {  // the top window missed: search the rest
+        top = L;
+        L = L0;
+        __syncthreads();
+        continue;
       }
-      __syncthreads();
-      return;
-    }
-    if ((int)top - HIST_BINS <= (int)lo) {
       if (tid == 0) {
         out[0] = 0;
         out[1] = deg;
@@ -324,7 +371,18 @@ __device__ __noinline__ void cta_window(const uint32_t* src, const EstT* snap, c
       __syncthreads();
       return;
     }
-    top -= HIST_BINS;
+    const uint32_t low = bin_low(top, w, L, g);
+    if (w == 1) {
+      if (found == g) {
+        out[0] = low;
+        out[1] = frun;
+      }
+      __syncthreads();
+      return;
+    }
+    top -= g * w;
+    L = low;
+    __syncthreads();
   }
 }
 
@@ -405,12 +463,12 @@ __device__ __noinline__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>
   uint32_t scanned = 0;
   if (it.list) {
     tc = warp_window<false>(p.radj, snap, s_cache, cache_n, bins, it.ob, it.ob + it.len, it.cap,
-                            lo > it.thr ? lo : it.thr, it.deg);
+                            lo > it.thr ? lo : it.thr, it.deg, !v.r0);
     scanned = it.len;
   }
   if (tc.x == 0) {  // no list, or the answer is below its threshold
     tc = warp_window<true>(p.adj, snap, s_cache, cache_n, bins, it.ob, it.ob + it.deg, it.cap, lo,
-                           it.deg);
+                           it.deg, !v.r0);
     scanned += it.deg;
   }
   if (lane_id() == 0) finish_eval(p, it, tc.x, tc.y, scanned, acc);
@@ -442,7 +500,7 @@ __device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>&
   uint32_t scanned = 0;
   if (it.list) {
     cta_window<false>(p.radj, snap, s_cache, cache_n, s_hist, sh.red, it.ob, it.ob + it.len,
-                      it.cap, lo > it.thr ? lo : it.thr, it.deg, sh.out);
+                      it.cap, lo > it.thr ? lo : it.thr, it.deg, !v.r0, sh.out);
     scanned = it.len;
   } else if (threadIdx.x == 0) {
     sh.out[0] = 0;
@@ -450,7 +508,7 @@ __device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>&
   __syncthreads();
   if (sh.out[0] == 0) {
     cta_window<true>(p.adj, snap, s_cache, cache_n, s_hist, sh.red, it.ob, it.ob + it.deg, it.cap,
-                     lo, it.deg, sh.out);
+                     lo, it.deg, !v.r0, sh.out);
     scanned += it.deg;
   }
   if (threadIdx.x == 0) finish_eval(p, it, sh.out[0], sh.out[1], scanned, acc);
@@ -550,6 +608,153 @@ __device__ __noinline__ void eval_wclass(const CP<OffT, EstT>& p, const View<Est
       it.ob = __shfl_sync(FULL, mine.ob, i);
       it.list = __shfl_sync(FULL, (uint32_t)mine.list, i) != 0;
       eval_warp(p, v, s_cache, bins, it, acc);
+    }
+  });
+}
+
+// ------------------------------------------------------------------------
+// Batched flat streams (rounds >= 1, BIG and WARP classes).  A warp takes G
+// queued vertices and streams their lists / rows CONCATENATED, 256 entries
+// per step, 8 consecutive entries per lane: every step keeps 8 id loads and
+// 8 gathers in flight per lane however short the rows are, and the per-vertex
+// work (window resolve, bookkeeping) is one lane's, not the warp's.
+//
+// Evaluate: for an active u, count(>= cap) = cnt[u] exactly (list or row) and
+// lo <= t < cap, so only values in [L, cap) are binned, L = max(lo, thr,
+// cap - FB); one lane per vertex then runs the suffix scan of
+// kernel.hpp:36-41 over its FB bins.  A vertex whose level lies below its
+// window takes the per-vertex windowed path afterwards.
+// Notify: the same stream over the droppers' lists against N.  Droppers
+// without a list (their first drop after round 0) take the per-vertex path,
+// which builds the list.
+// ------------------------------------------------------------------------
+struct FlatW {                // per-warp batch state (shared memory)
+  uint32_t pre[33];           // exclusive prefix of the segment lengths; pre[n] = total
+  uint32_t hi[32];            // evaluate: cap; notify: cap (old estimate)
+  uint32_t lo[32];            // evaluate: window floor L; notify: t (new estimate)
+  uint32_t list[32];          // segment reads radj (1) or adj (0)
+  unsigned long long ob[32];  // segment start in adj / radj
+};
+
+__device__ __forceinline__ uint32_t flat_fb(uint32_t G) {  // bins per vertex
+  return G <= 1u ? (uint32_t)WARP_BINS : (uint32_t)WARP_BINS >> (32 - __clz(G - 1u));
+}
+
+// Stream the batch: f(seg[8], ids[8], x[8], ok) per step.
+template <typename OffT, typename EstT, typename F>
+__device__ __forceinline__ void flat_stream(const CP<OffT, EstT>& p, const FlatW& fw, uint32_t n,
+                                            const EstT* snap, const EstT* s_cache,
+                                            uint32_t cache_n, F&& f) {
+  const uint32_t lane = lane_id();
+  const uint32_t total = fw.pre[n];
+  for (uint32_t base = 0; base < total; base += 256) {
+    const uint32_t first = base + 8 * lane;
+    uint32_t s = 0;
+    if (first < total) {  // segment of `first`: largest s with pre[s] <= first
+      uint32_t a = 0, b = n;
+      while (b - a > 1) {
+        const uint32_t mid = (a + b) >> 1;
+        if (fw.pre[mid] <= first) a = mid; else b = mid;
+      }
+      s = a;
+    }
+    uint32_t seg[8], ids[8], x[8], ok = 0;
+    uint32_t s_pre = fw.pre[s], s_end = fw.pre[s + 1];
+    const uint32_t* s_src = fw.list[s] ? p.radj : p.adj;
+    uint64_t s_ob = fw.ob[s];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t e = first + j;
+      const bool val = e < total;
+      if (val && e >= s_end) {  // next non-empty segment
+        do { ++s; } while (e >= fw.pre[s + 1]);
+        s_pre = fw.pre[s];
+        s_end = fw.pre[s + 1];
+        s_src = fw.list[s] ? p.radj : p.adj;
+        s_ob = fw.ob[s];
+      }
+      seg[j] = s;
+      ok |= (uint32_t)val << j;
+      ids[j] = val ? __ldcg(s_src + s_ob + (e - s_pre)) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = (ok >> j & 1) ? est_at(s_cache, cache_n, snap, ids[j]) : 0u;
+    f(seg, ids, x, ok);
+  }
+}
+
+template <typename OffT, typename EstT>
+__device__ __noinline__ void flat_eval(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                       const EstT* s_cache, uint32_t* bins, FlatW& fw, int c,
+                                       uint32_t gmax, Acc& acc) {
+  const uint32_t lane = lane_id();
+  const EstT* snap = v.snap;
+  const uint32_t cache_n = v.cache_n;
+  const uint32_t fb = flat_fb(grab_size(v.qcnt[c], gmax));
+  for_class(p, v, c, gmax, [&](uint32_t u, uint32_t n) {
+    Item it{};
+    uint32_t L = 0;
+    if (lane < n) {
+      it = eval_item(p, v, s_cache, u);
+      L = it.lo;
+      if (it.list && it.thr > L) L = it.thr;
+      if (it.cap > fb && it.cap - fb > L) L = it.cap - fb;
+      if (L < 1u) L = 1u;
+    }
+    const uint32_t len = lane < n ? it.len : 0u;
+    const uint32_t incl = warp_incl_scan(len);
+    fw.pre[lane] = incl - len;
+    if (lane == 31) fw.pre[32] = incl;
+    fw.hi[lane] = it.cap;
+    fw.lo[lane] = L;
+    fw.list[lane] = it.list ? 1u : 0u;
+    fw.ob[lane] = it.ob;
+    for (uint32_t i = lane; i < (uint32_t)WARP_BINS; i += 32) bins[i] = 0;
+    __syncwarp();
+    if (n < 32 && lane == 0) fw.pre[n] = fw.pre[32];
+    __syncwarp();
+    flat_stream(p, fw, n, snap, s_cache, cache_n,
+                [&](const uint32_t(&seg)[8], const uint32_t(&)[8], const uint32_t(&x)[8],
+                    uint32_t ok) {
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) {
+                    if (!(ok >> j & 1)) continue;
+                    const uint32_t sj = seg[j];
+                    const uint32_t cp = fw.hi[sj];
+                    if (x[j] < cp && x[j] >= fw.lo[sj]) atomicAdd(&bins[sj * fb + (cp - 1 - x[j])], 1u);
+                  }
+                });
+    __syncwarp();
+    // one lane per vertex: suffix scan of its window (C = count(>= cap) = lo)
+    bool deep = false;
+    if (lane < n) {
+      uint32_t run = it.lo, t = 0;
+      for (uint32_t k = 0; k < fb && it.cap - k > L; ++k) {
+        const uint32_t level = it.cap - 1 - k;
+        run += bins[lane * fb + k];
+        if (run >= level) {
+          t = level;
+          break;
+        }
+      }
+      if (t) finish_eval(p, it, t, run, it.len, acc);
+      else deep = true;  // below the window: per-vertex passes
+    }
+    uint32_t dm = __ballot_sync(FULL, deep);
+    __syncwarp();
+    while (dm) {
+      const int i = __ffs(dm) - 1;
+      dm &= dm - 1;
+      Item d;
+      d.u = __shfl_sync(FULL, it.u, i);
+      d.cap = __shfl_sync(FULL, it.cap, i);
+      d.lo = __shfl_sync(FULL, it.lo, i);
+      d.thr = __shfl_sync(FULL, it.thr, i);
+      d.len = __shfl_sync(FULL, it.len, i);
+      d.deg = __shfl_sync(FULL, it.deg, i);
+      d.ob = __shfl_sync(FULL, it.ob, i);
+      d.list = __shfl_sync(FULL, (uint32_t)it.list, i) != 0;
+      eval_warp(p, v, s_cache, bins, d, acc);
     }
   });
 }
@@ -807,6 +1012,77 @@ __device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p, const View<E
   if (lane_id() == 0) acc.nscan += nscan;
 }
 
+template <typename OffT, typename EstT>
+__device__ __noinline__ void flat_notify(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                         const Enq& q, const EstT* s_cache, FlatW& fw, int c,
+                                         uint32_t gmax, Acc& acc) {
+  const uint32_t lane = lane_id();
+  const uint32_t cache_n = v.cache_n;
+  uint32_t fires = 0, nscan = 0;
+  for_class(p, v, c, gmax, [&](uint32_t u, uint32_t n) {
+    Drop d{};
+    if (lane < n) d = drop_item(p, u);  // rounds >= 1: every queued vertex dropped
+    const bool flat = lane < n && d.thr != 0;  // has a list: stream it in the batch
+    const uint32_t len = flat ? d.len : 0u;
+    const uint32_t incl = warp_incl_scan(len);
+    fw.pre[lane] = incl - len;
+    if (lane == 31) fw.pre[32] = incl;
+    fw.hi[lane] = d.cap;
+    fw.lo[lane] = d.t;
+    fw.list[lane] = 1u;
+    fw.ob[lane] = d.ob;
+    __syncwarp();
+    if (n < 32 && lane == 0) fw.pre[n] = fw.pre[32];
+    __syncwarp();
+    nscan += len;
+    flat_stream(p, fw, n, (const EstT*)p.N, s_cache, cache_n,
+                [&](const uint32_t(&seg)[8], const uint32_t(&ids)[8], const uint32_t(&x)[8],
+                    uint32_t ok) {
+                  uint32_t fire = 0;
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) {
+                    const uint32_t sj = seg[j];
+                    const bool f = (ok >> j & 1) && fw.lo[sj] < x[j] && x[j] <= fw.hi[sj];
+                    fire |= (uint32_t)f << j;
+                  }
+                  uint32_t act = 0;
+                  if (fire) {
+                    fires += __popc(fire);
+                    uint32_t old[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                      old[j] = (fire >> j & 1) ? atomicSub(&p.cnt[ids[j]], 1u) : 0u;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) act |= (uint32_t)((fire >> j & 1) && old[j] == x[j]) << j;
+                  }
+                  if (__any_sync(FULL, act)) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                      if (__any_sync(FULL, act >> j & 1)) wq_push(p, q, (act >> j & 1) != 0, ids[j]);
+                  }
+                });
+    if (flat) p.E[d.u] = (EstT)d.t;  // apply (fastk.cpp:153)
+    // droppers without a list: per-vertex pass that builds it
+    uint32_t rest = __ballot_sync(FULL, lane < n && !flat);
+    while (rest) {
+      const int i = __ffs(rest) - 1;
+      rest &= rest - 1;
+      Drop e;
+      e.u = __shfl_sync(FULL, d.u, i);
+      e.t = __shfl_sync(FULL, d.t, i);
+      e.cap = __shfl_sync(FULL, d.cap, i);
+      e.thr = __shfl_sync(FULL, d.thr, i);
+      e.len = __shfl_sync(FULL, d.len, i);
+      e.deg = __shfl_sync(FULL, d.deg, i);
+      e.ob = __shfl_sync(FULL, d.ob, i);
+      fires += notify_drop_warp(p, q, s_cache, cache_n, false, e);
+      if (lane == 0) nscan += e.len;
+    }
+  });
+  acc.fires += fires;
+  acc.nscan += nscan;
+}
+
 // SUB and THREAD droppers: 8-lane tile per dropper, up to 8 neighbours per lane.
 template <typename OffT, typename EstT>
 __device__ __noinline__ void notify_small(const CP<OffT, EstT>& p, const View<EstT>& v,
@@ -879,6 +1155,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
   uint32_t* w_bins = s_hist + WARP_BINS * warp_id();
   uint32_t* s_wq = s_hist + HREG;  // per-warp enqueue buffers
   __shared__ uint32_t s_wn[NWARPS][NCLS];
+  __shared__ FlatW s_flat[(KC_FLAT_EVAL || KC_FLAT_NOTIFY) ? NWARPS : 1];
   __shared__ Shared sh;
   uint32_t* wn = s_wn[warp_id()];
   const uint32_t tid = threadIdx.x;
@@ -950,8 +1227,13 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
         });
     consume_long(p, v, sh, ctl, 0, false, eval_long);
     if (pf) pf[2] = gtimer();
-    eval_wclass(p, v, s_cache, w_bins, C_BIG, GMAX_BIG, acc);
-    eval_wclass(p, v, s_cache, w_bins, C_WARP, GMAX_WARP, acc);
+    if (v.r0 || !KC_FLAT_EVAL) {
+      eval_wclass(p, v, s_cache, w_bins, C_BIG, GMAX_BIG, acc);
+      eval_wclass(p, v, s_cache, w_bins, C_WARP, GMAX_WARP, acc);
+    } else {
+      flat_eval(p, v, s_cache, w_bins, s_flat[warp_id()], C_BIG, GMAX_BIG, acc);
+      flat_eval(p, v, s_cache, w_bins, s_flat[warp_id()], C_WARP, GMAX_WARP, acc);
+    }
     if (pf) pf[3] = gtimer();
     eval_sub(p, v, s_cache, acc);
     eval_thread(p, v, s_cache, acc);
@@ -1007,8 +1289,13 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
           }
         });
     consume_long(p, v, sh, ctl, 1, false, notify_long);
-    notify_wclass(p, v, q, s_cache, C_BIG, GMAX_BIG, acc);
-    notify_wclass(p, v, q, s_cache, C_WARP, GMAX_WARP, acc);
+    if (v.r0 || !KC_FLAT_NOTIFY) {
+      notify_wclass(p, v, q, s_cache, C_BIG, GMAX_BIG, acc);
+      notify_wclass(p, v, q, s_cache, C_WARP, GMAX_WARP, acc);
+    } else {
+      flat_notify(p, v, q, s_cache, s_flat[warp_id()], C_BIG, GMAX_BIG, acc);
+      flat_notify(p, v, q, s_cache, s_flat[warp_id()], C_WARP, GMAX_WARP, acc);
+    }
     notify_small(p, v, q, s_cache, C_SUB, acc);
     notify_small(p, v, q, s_cache, C_THREAD, acc);
     consume_long(p, v, sh, ctl, 1, true, notify_long);

@@ -204,6 +204,47 @@ __device__ __forceinline__ bool warp_resolve(const uint32_t* bins, uint32_t C, u
   return true;
 }
 
+// Coarse windows.  The levels [L, top) are split into bins of width w, bin i
+// covering [low_i, top - i*w) with low_i = max(top - (i+1)*w, L), i = 0 at
+// the top; C = count(>= top).  count(>= low_i) = C + bins[0..i] =: run_i,
+// so the largest qualifying level (count(>= x) >= x) lies in the first bin
+// with run_i >= low_i, and no level above it qualifies.  Warp version, lane l
+// owns bins [8l, 8l+8).  Returns that bin and run_i.
+__device__ __forceinline__ uint32_t bin_low(uint32_t top, uint32_t w, uint32_t L, uint32_t i) {
+  const uint64_t d = (uint64_t)(i + 1) * w;
+  return d >= (uint64_t)(top - L) ? L : top - (uint32_t)d;
+}
+
+__device__ __forceinline__ bool warp_resolve_w(const uint32_t* bins, uint32_t C, uint32_t top,
+                                               uint32_t w, uint32_t L, uint32_t& bin,
+                                               uint32_t& run_at) {
+  static_assert(WARP_BINS == 256, "8 bins per lane");
+  const uint32_t lane = lane_id();
+  const uint4 b0 = reinterpret_cast<const uint4*>(bins)[2 * lane];
+  const uint4 b1 = reinterpret_cast<const uint4*>(bins)[2 * lane + 1];
+  const uint32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += b[j];
+  uint32_t run = C + warp_incl_scan(s) - s;
+  const uint32_t nb = (top - L + w - 1) / w;  // bins in use
+  uint32_t found = 0xffffffffu, frun = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    run += b[j];
+    const uint32_t i = lane * 8 + j;
+    if (found == 0xffffffffu && i < nb && run >= bin_low(top, w, L, i)) {
+      found = i;
+      frun = run;
+    }
+  }
+  const uint32_t g = __reduce_min_sync(FULL, found);
+  if (g == 0xffffffffu) return false;
+  run_at = __shfl_sync(FULL, frun, g >> 3);
+  bin = g;
+  return true;
+}
+
 __device__ __forceinline__ void warp_zero_bins(uint32_t* bins) {
   const uint32_t lane = lane_id();
   reinterpret_cast<uint4*>(bins)[2 * lane] = make_uint4(0, 0, 0, 0);
