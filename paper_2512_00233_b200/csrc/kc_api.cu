@@ -167,6 +167,7 @@ void free_solver(kc_graph* g) {
   dfree(g->sb.radj, g->stream);
   dfree(g->sb.rlen, g->stream);
   dfree(g->sb.rthr, g->stream);
+  dfree(g->sb.spec, g->stream);
   dfree(g->sb.lq[0], g->stream);
   dfree(g->sb.lq[1], g->stream);
   dfree(g->sb.flag[0], g->stream);
@@ -207,6 +208,8 @@ kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
   CK(dmalloc((void**)&b.rthr, n_pad * es, g->stream));
   CK(dmalloc((void**)&b.radj, ((size_t)g->nnz + ADJ_PAD) * sizeof(uint32_t), g->stream));
   CK(cudaMemsetAsync(b.radj + g->nnz, 0, ADJ_PAD * sizeof(uint32_t), g->stream));
+  CK(dmalloc((void**)&b.spec, 3 * ((((size_t)n_nz + 15) & ~(size_t)15) + 16) * sizeof(uint32_t),
+             g->stream));
   for (int ph = 0; ph < 2; ++ph) {  // slots hold 0xffffffff while empty
     CK(dmalloc((void**)&b.lq[ph], ((size_t)b.cls_begin[1] + 1) * sizeof(uint32_t), g->stream));
     CK(cudaMemsetAsync(b.lq[ph], 0xff, ((size_t)b.cls_begin[1] + 1) * sizeof(uint32_t), g->stream));

@@ -69,6 +69,12 @@ constexpr int WQ = 64;             // per-warp, per-class enqueue buffer (flushe
 #ifndef KC_FLAT_NOTIFY
 #define KC_FLAT_NOTIFY 0           // ... and notify (slower: per-entry segment lookups)
 #endif
+#ifndef KC_SPEC
+#define KC_SPEC 1                  // notify scans evaluate droppers for the next round
+#endif
+#ifndef KC_SPEC_BINS
+#define KC_SPEC_BINS 256           // spec window width (levels below t), <= WARP_BINS
+#endif
 #ifndef KC_R0_PASSA
 #define KC_R0_PASSA 0              // 1: round 0 first counts values >= cap (one pass when
 #endif                             //    nothing drops); 0: straight to the window
@@ -86,6 +92,9 @@ struct CP {
   uint32_t* radj;       // relevant-neighbour lists, row u at off[u]
   uint32_t* rlen;       // list lengths
   EstT* rthr;           // list thresholds L_u (0: no list, use the CSR row)
+  uint32_t* spec_r;     // speculative next-round evaluation: round it is valid for,
+  uint32_t* spec_t;     //   its level and
+  uint32_t* spec_c;     //   count(>= level) (computed by the notify scan, see NOTIFY)
   uint32_t n_nz;
   uint32_t cb[NCLS + 1];
   EstT* E;  // snapshot
@@ -111,6 +120,7 @@ struct View {
   uint32_t* qnext;       // next round's queue
   uint32_t cache_n;      // ids cached in shared memory this phase (0: none)
   bool r0;
+  uint32_t round;
 };
 
 struct Acc {  // per-thread counters, flushed per round
@@ -408,6 +418,8 @@ struct Item {
   uint32_t u, cap, lo, thr, len, deg;
   uint64_t ob;
   bool list;
+  bool spec;               // evaluated in advance by last round's notify scan
+  uint32_t spec_t, spec_c;
 };
 
 // A vertex with a list (thr != 0) is first evaluated on it: levels >= thr
@@ -424,7 +436,10 @@ __device__ __forceinline__ Item eval_item(const CP<OffT, EstT>& p, const View<Es
   it.lo = v.r0 ? 0u : p.cnt[u];
   it.thr = (v.r0 || it.deg <= LIST_MIN_DEG) ? 0u : (uint32_t)p.rthr[u];
   it.list = it.thr != 0;
-  it.len = it.list ? p.rlen[u] : it.deg;
+  it.spec = !v.r0 && it.deg > LIST_MIN_DEG && p.spec_r[u] == v.round;
+  it.spec_t = it.spec ? p.spec_t[u] : 0u;
+  it.spec_c = it.spec ? p.spec_c[u] : 0u;
+  it.len = it.spec ? 0u : it.list ? p.rlen[u] : it.deg;
   return it;
 }
 
@@ -448,6 +463,10 @@ __device__ __forceinline__ void finish_eval(const CP<OffT, EstT>& p, const Item&
 template <typename OffT, typename EstT>
 __device__ __noinline__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                           uint32_t* bins, const Item& it, Acc& acc) {
+  if (it.spec) {
+    if (lane_id() == 0) finish_eval(p, it, it.spec_t, it.spec_c, 0u, acc);
+    return;
+  }
   const EstT* snap = v.snap;
   const uint32_t cache_n = v.cache_n;
   uint32_t lo = it.lo;
@@ -478,6 +497,11 @@ template <typename OffT, typename EstT>
 __device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                          uint32_t* s_hist, Shared& sh, uint32_t u, Acc& acc) {
   const Item it = eval_item(p, v, s_cache, u);
+  if (it.spec) {
+    if (threadIdx.x == 0) finish_eval(p, it, it.spec_t, it.spec_c, 0u, acc);
+    __syncthreads();
+    return;
+  }
   const EstT* snap = v.snap;
   const uint32_t cache_n = v.cache_n;
   uint32_t lo = it.lo;
@@ -607,6 +631,9 @@ __device__ __noinline__ void eval_wclass(const CP<OffT, EstT>& p, const View<Est
       it.deg = __shfl_sync(FULL, mine.deg, i);
       it.ob = __shfl_sync(FULL, mine.ob, i);
       it.list = __shfl_sync(FULL, (uint32_t)mine.list, i) != 0;
+      it.spec = __shfl_sync(FULL, (uint32_t)mine.spec, i) != 0;
+      it.spec_t = __shfl_sync(FULL, mine.spec_t, i);
+      it.spec_c = __shfl_sync(FULL, mine.spec_c, i);
       eval_warp(p, v, s_cache, bins, it, acc);
     }
   });
@@ -701,7 +728,9 @@ __device__ __noinline__ void flat_eval(const CP<OffT, EstT>& p, const View<EstT>
       if (it.cap > fb && it.cap - fb > L) L = it.cap - fb;
       if (L < 1u) L = 1u;
     }
-    const uint32_t len = lane < n ? it.len : 0u;
+    if (lane < n && it.spec) finish_eval(p, it, it.spec_t, it.spec_c, 0u, acc);
+    const bool pending = lane < n && !it.spec;
+    const uint32_t len = pending ? it.len : 0u;
     const uint32_t incl = warp_incl_scan(len);
     fw.pre[lane] = incl - len;
     if (lane == 31) fw.pre[32] = incl;
@@ -727,7 +756,7 @@ __device__ __noinline__ void flat_eval(const CP<OffT, EstT>& p, const View<EstT>
     __syncwarp();
     // one lane per vertex: suffix scan of its window (C = count(>= cap) = lo)
     bool deep = false;
-    if (lane < n) {
+    if (pending) {
       uint32_t run = it.lo, t = 0;
       for (uint32_t k = 0; k < fb && it.cap - k > L; ++k) {
         const uint32_t level = it.cap - 1 - k;
@@ -754,6 +783,7 @@ __device__ __noinline__ void flat_eval(const CP<OffT, EstT>& p, const View<EstT>
       d.deg = __shfl_sync(FULL, it.deg, i);
       d.ob = __shfl_sync(FULL, it.ob, i);
       d.list = __shfl_sync(FULL, (uint32_t)it.list, i) != 0;
+      d.spec = false;
       eval_warp(p, v, s_cache, bins, d, acc);
     }
   });
@@ -870,19 +900,40 @@ __device__ __forceinline__ uint32_t list_threshold(uint32_t t) {
   return L ? L : 1u;
 }
 
+// The notify scan gathers N over u's list — exactly the snapshot u's next
+// evaluation would read (E of round r+1 = N of round r; N is not written
+// during notify).  So the scan also evaluates u for round r+1 (`tag`):
+// values >= t counted, [max(t - NB, floor), t) binned, suffix scan; the
+// result is kept in spec_* and the next evaluate phase takes it instead of
+// rescanning (it is used only if u is activated, which happens iff the
+// level is below t).  floor = the list threshold (levels below it are not
+// decided by the list) or 1.
+
 // Returns the notifications fired by this lane (counted once per warp in
 // `acc` by the callers).
 template <bool RO, typename OffT, typename EstT>
 __device__ __noinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const Enq& q,
                                              const EstT* s_cache, uint32_t cache_n,
-                                             const uint32_t* src, uint32_t u, uint64_t ob,
-                                             uint32_t len, uint32_t t, uint32_t cap,
-                                             uint32_t build) {
+                                             uint32_t* bins, const uint32_t* src, uint32_t u,
+                                             uint64_t ob, uint32_t len, uint32_t t, uint32_t cap,
+                                             uint32_t build, uint32_t tag, uint32_t floor) {
   uint32_t cursor = 0;  // warp-uniform
   uint32_t fires = 0;
+  uint32_t above = 0;
+  const uint32_t sl = t > (uint32_t)KC_SPEC_BINS ? t - KC_SPEC_BINS : 1u;
+  const uint32_t slo = floor > sl ? floor : sl;  // spec window [slo, t)
+  if (tag) warp_zero_bins(bins);
   stream_row<32, RO>(src, p.N, lane_id(), ob, ob + len, s_cache, cache_n,
                      [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
                        notify8(p, q, ok, ids, x, t, cap, fires);
+                       if (tag) {
+#pragma unroll
+                         for (int k = 0; k < 8; ++k) {
+                           if (!(ok >> k & 1)) continue;
+                           if (x[k] >= t) ++above;
+                           else if (x[k] >= slo) atomicAdd(&bins[t - 1 - x[k]], 1u);
+                         }
+                       }
                        if (build) {
                          uint32_t keep = 0;
 #pragma unroll
@@ -896,6 +947,23 @@ __device__ __noinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const Enq&
                          cursor += __shfl_sync(FULL, incl, 31);
                        }
                      });
+  if (tag) {
+    __syncwarp();
+    const uint32_t C = __reduce_add_sync(FULL, above);
+    uint32_t lvl = t, cnt = C, b = 0, run = 0;
+    bool ok = C >= t;  // no drop next round (u will not be activated)
+    if (!ok && t > slo && warp_resolve_w(bins, C, t, 1u, slo, b, run)) {
+      ok = true;
+      lvl = t - 1 - b;
+      cnt = run;
+    }
+    if (ok && lane_id() == 0) {
+      p.spec_t[u] = lvl;
+      p.spec_c[u] = cnt;
+      p.spec_r[u] = tag;
+    }
+    __syncwarp();
+  }
   if (lane_id() == 0) {
     if (build) {
       p.rlen[u] = cursor;
@@ -909,15 +977,28 @@ __device__ __noinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const Enq&
 template <bool RO, typename OffT, typename EstT>
 __device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p, const Enq& q,
                                             const EstT* s_cache, uint32_t cache_n, Shared& sh,
-                                            const uint32_t* src, uint32_t u, uint64_t ob,
-                                            uint32_t len, uint32_t t, uint32_t cap,
-                                            uint32_t build) {
-  if (threadIdx.x == 0) sh.cursor = 0;
+                                            uint32_t* s_hist, const uint32_t* src, uint32_t u,
+                                            uint64_t ob, uint32_t len, uint32_t t, uint32_t cap,
+                                            uint32_t build, uint32_t tag, uint32_t floor) {
+  const uint32_t tid = threadIdx.x;
+  if (tid == 0) sh.cursor = 0;
+  const uint32_t sl = t > (uint32_t)KC_SPEC_BINS ? t - KC_SPEC_BINS : 1u;
+  const uint32_t slo = floor > sl ? floor : sl;
+  if (tag)
+    for (int i = tid; i < HIST_BINS; i += SOLVE_THREADS) s_hist[i] = 0;
   __syncthreads();
-  uint32_t fires = 0;
-  stream_row<SOLVE_THREADS, RO>(src, p.N, threadIdx.x, ob, ob + len, s_cache, cache_n,
+  uint32_t fires = 0, above = 0;
+  stream_row<SOLVE_THREADS, RO>(src, p.N, tid, ob, ob + len, s_cache, cache_n,
                                 [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
                                   notify8(p, q, ok, ids, x, t, cap, fires);
+                                  if (tag) {
+#pragma unroll
+                                    for (int k = 0; k < 8; ++k) {
+                                      if (!(ok >> k & 1)) continue;
+                                      if (x[k] >= t) ++above;
+                                      else if (x[k] >= slo) atomicAdd(&s_hist[t - 1 - x[k]], 1u);
+                                    }
+                                  }
                                   if (build) {
                                     uint32_t keep = 0;
 #pragma unroll
@@ -934,8 +1015,44 @@ __device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p, const Enq& 
                                       if (keep >> k & 1) p.radj[ob + pos++] = ids[k];
                                   }
                                 });
+  if (tag) {  // CTA suffix scan of the spec window (one pass, no refinement)
+    const uint32_t C = block_sum(above, sh.red);
+    constexpr int PER = (HIST_BINS + SOLVE_THREADS - 1) / SOLVE_THREADS;
+    uint32_t h[PER];
+    uint32_t sm = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      h[j] = tid * PER + j < HIST_BINS ? s_hist[tid * PER + j] : 0u;
+      sm += h[j];
+    }
+    uint32_t run = C + block_excl_scan(sm, sh.red);
+    uint32_t found = 0xffffffffu, frun = 0;
+    if (C < t) {
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        run += h[j];
+        const uint32_t i = tid * PER + j;
+        if (found == 0xffffffffu && i < t - slo && run >= t - 1 - i) {
+          found = i;
+          frun = run;
+        }
+      }
+    }
+    const uint32_t g = block_min(found, sh.red);
+    if (C >= t) {
+      if (tid == 0) {
+        p.spec_t[u] = t;
+        p.spec_c[u] = C;
+        p.spec_r[u] = tag;
+      }
+    } else if (g != 0xffffffffu && found == g) {
+      p.spec_t[u] = t - 1 - g;
+      p.spec_c[u] = frun;
+      p.spec_r[u] = tag;
+    }
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     if (build) {
       p.rlen[u] = sh.cursor;
       p.rthr[u] = (EstT)build;
@@ -975,18 +1092,20 @@ __device__ __forceinline__ uint32_t list_build(bool r0, const Drop& d) {
 template <typename OffT, typename EstT>
 __device__ __forceinline__ uint32_t notify_drop_warp(const CP<OffT, EstT>& p, const Enq& q,
                                                      const EstT* s_cache, uint32_t cache_n,
-                                                     bool r0, const Drop& d) {
+                                                     uint32_t* bins, uint32_t round,
+                                                     const Drop& d) {
+  const uint32_t tag = KC_SPEC ? round + 1 : 0u;
   if (d.thr)  // optionally in place: drop entries whose settled value fell below the threshold
-    return notify_warp<false>(p, q, s_cache, cache_n, p.radj, d.u, d.ob, d.len, d.t, d.cap,
-                              KC_LIST_COMPACT ? d.thr : 0u);
-  return notify_warp<true>(p, q, s_cache, cache_n, p.adj, d.u, d.ob, d.len, d.t, d.cap,
-                           list_build(r0, d));
+    return notify_warp<false>(p, q, s_cache, cache_n, bins, p.radj, d.u, d.ob, d.len, d.t, d.cap,
+                              KC_LIST_COMPACT ? d.thr : 0u, tag, d.thr);
+  return notify_warp<true>(p, q, s_cache, cache_n, bins, p.adj, d.u, d.ob, d.len, d.t, d.cap,
+                           list_build(round == 0, d), tag, 1u);
 }
 
 template <typename OffT, typename EstT>
 __device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p, const View<EstT>& v,
-                                           const Enq& q, const EstT* s_cache, int c,
-                                           uint32_t gmax, Acc& acc) {
+                                           const Enq& q, const EstT* s_cache, uint32_t* bins,
+                                           int c, uint32_t gmax, Acc& acc) {
   const uint32_t cache_n = v.cache_n;
   const bool r0 = v.r0;
   uint32_t fires = 0;
@@ -1004,7 +1123,7 @@ __device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p, const View<E
       d.len = __shfl_sync(FULL, mine.len, i);
       d.deg = __shfl_sync(FULL, mine.deg, i);
       d.ob = __shfl_sync(FULL, mine.ob, i);
-      fires += notify_drop_warp(p, q, s_cache, cache_n, r0, d);
+      fires += notify_drop_warp(p, q, s_cache, cache_n, bins, v.round, d);
       nscan += d.len;
     }
   });
@@ -1014,8 +1133,8 @@ __device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p, const View<E
 
 template <typename OffT, typename EstT>
 __device__ __noinline__ void flat_notify(const CP<OffT, EstT>& p, const View<EstT>& v,
-                                         const Enq& q, const EstT* s_cache, FlatW& fw, int c,
-                                         uint32_t gmax, Acc& acc) {
+                                         const Enq& q, const EstT* s_cache, uint32_t* bins,
+                                         FlatW& fw, int c, uint32_t gmax, Acc& acc) {
   const uint32_t lane = lane_id();
   const uint32_t cache_n = v.cache_n;
   uint32_t fires = 0, nscan = 0;
@@ -1075,7 +1194,7 @@ __device__ __noinline__ void flat_notify(const CP<OffT, EstT>& p, const View<Est
       e.len = __shfl_sync(FULL, d.len, i);
       e.deg = __shfl_sync(FULL, d.deg, i);
       e.ob = __shfl_sync(FULL, d.ob, i);
-      fires += notify_drop_warp(p, q, s_cache, cache_n, false, e);
+      fires += notify_drop_warp(p, q, s_cache, cache_n, bins, v.round, e);
       if (lane == 0) nscan += e.len;
     }
   });
@@ -1179,6 +1298,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     q.qn = v.qn;
     q.qnext = v.qnext;
     v.r0 = r == 0;
+    v.round = r;
     unsigned long long* pf = (p.prof && r < PROF_ROUNDS && tid == 0)
                                  ? p.prof + ((size_t)r * gridDim.x + blockIdx.x) * PROF_PHASES
                                  : nullptr;
@@ -1268,10 +1388,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     auto notify_long = [&](uint32_t u) {
       const Drop d = drop_item(p, u);  // a long-queued hub always dropped
       const uint32_t f =
-          d.thr ? notify_cta<false>(p, q, s_cache, cache_n, sh, p.radj, d.u, d.ob, d.len, d.t,
-                                    d.cap, 0u)
-                : notify_cta<true>(p, q, s_cache, cache_n, sh, p.adj, d.u, d.ob, d.len, d.t,
-                                   d.cap, list_build(v.r0, d));
+          d.thr ? notify_cta<false>(p, q, s_cache, cache_n, sh, s_hist, p.radj, d.u, d.ob, d.len,
+                                    d.t, d.cap, 0u, KC_SPEC ? r + 1 : 0u, d.thr)
+                : notify_cta<true>(p, q, s_cache, cache_n, sh, s_hist, p.adj, d.u, d.ob, d.len,
+                                   d.t, d.cap, list_build(v.r0, d), KC_SPEC ? r + 1 : 0u, 1u);
       acc.fires += f;
       if (tid == 0) acc.nscan += d.len;
     };
@@ -1284,17 +1404,17 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
         [&](uint32_t u) {
           const Drop d = drop_item(p, u);
           if (d.t < d.cap) {
-            acc.fires += notify_drop_warp(p, q, s_cache, cache_n, v.r0, d);
+            acc.fires += notify_drop_warp(p, q, s_cache, cache_n, w_bins, r, d);
             if (lane_id() == 0) acc.nscan += d.len;
           }
         });
     consume_long(p, v, sh, ctl, 1, false, notify_long);
     if (v.r0 || !KC_FLAT_NOTIFY) {
-      notify_wclass(p, v, q, s_cache, C_BIG, GMAX_BIG, acc);
-      notify_wclass(p, v, q, s_cache, C_WARP, GMAX_WARP, acc);
+      notify_wclass(p, v, q, s_cache, w_bins, C_BIG, GMAX_BIG, acc);
+      notify_wclass(p, v, q, s_cache, w_bins, C_WARP, GMAX_WARP, acc);
     } else {
-      flat_notify(p, v, q, s_cache, s_flat[warp_id()], C_BIG, GMAX_BIG, acc);
-      flat_notify(p, v, q, s_cache, s_flat[warp_id()], C_WARP, GMAX_WARP, acc);
+      flat_notify(p, v, q, s_cache, w_bins, s_flat[warp_id()], C_BIG, GMAX_BIG, acc);
+      flat_notify(p, v, q, s_cache, w_bins, s_flat[warp_id()], C_WARP, GMAX_WARP, acc);
     }
     notify_small(p, v, q, s_cache, C_SUB, acc);
     notify_small(p, v, q, s_cache, C_THREAD, acc);
@@ -1327,6 +1447,7 @@ __global__ void count_init_kernel(CP<OffT, EstT> p, uint32_t h_graph, uint32_t n
     p.N[u] = e;
     p.cnt[u] = 0;
     p.rthr[u] = 0;
+    p.spec_r[u] = 0;
   }
   for (uint32_t k = gtid; k < STAT_SLOTS * (uint32_t)(sizeof(RoundStat) / 8); k += gsize)
     reinterpret_cast<unsigned long long*>(p.stats)[k] = 0;
@@ -1349,6 +1470,10 @@ CP<OffT, EstT> make_params(const SolveBuffers& b) {
   p.radj = b.radj;
   p.rlen = b.rlen;
   p.rthr = static_cast<EstT*>(b.rthr);
+  const size_t n_pad = ((size_t)b.n_nz + 15) & ~(size_t)15;
+  p.spec_r = b.spec;
+  p.spec_t = b.spec + n_pad;
+  p.spec_c = b.spec + 2 * n_pad;
   p.n_nz = b.n_nz;
   for (int c = 0; c <= NCLS; ++c) p.cb[c] = b.cls_begin[c];
   p.E = static_cast<EstT*>(b.est[0]);

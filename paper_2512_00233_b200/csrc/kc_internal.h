@@ -70,6 +70,8 @@ struct SolveBuffers {
   uint32_t* rlen;            // counting rule: list lengths [n_pad]
   void* rthr;                // counting rule: list thresholds (EstT) [n_pad]
   uint32_t* lq[2];           // counting rule: long-scan queues per phase [cls_begin[1]]
+  uint32_t* spec;            // counting rule: next-round evaluations [3][n_pad16]
+                             // (round tag, level, count), n_pad16 = n_nz rounded to 16
   Ctl* ctl;                  // [2]
   uint32_t* anydrop;         // [3] "some estimate dropped in round r" (r % 3)
   RoundStat* stats;          // [STAT_SLOTS]
