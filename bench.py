@@ -17,7 +17,7 @@ e2e     = the same metric through the public C-ABI call with HOST buffers:
           pinned CSR -> kc_graph_upload (H2D + layout) -> kc_solve -> coreness
           on the host, per step.
 roofline= algorithmic bytes (8 * E_scan + 16 * V_eval of the run)
-          / rounds-kernel time vs MEASURED_PEAKS.json hbm_gbs.
+          / solver-kernel time vs MEASURED_PEAKS.json hbm_gbs.
 """
 from __future__ import annotations
 
@@ -154,13 +154,18 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic(cfg: int):
-    """DRAM bytes per launch of the rounds kernel from the committed ncu capture."""
+def solver_kernel(rule: int) -> str:
+    """The persistent kernel that runs the rounds for this rule."""
+    return "rounds_kernel" if rule == 0 else "count_rounds_kernel"
+
+
+def profile_traffic(cfg: int, kernel: str):
+    """DRAM bytes per launch of the solver kernel from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        v = d.get(f"cfg{cfg}", {}).get("rounds_kernel", {})
+        v = d.get(f"cfg{cfg}", {}).get(kernel, {})
         return v.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
@@ -237,7 +242,8 @@ def run_ours(args, ws, rank, local):
     peak, peak_src = measured_peak()
     bytes_alg = 8 * e_our + 16 * v_our
     achieved = bytes_alg / (ms_step * 1e-3) / 1e9
-    traffic = profile_traffic(args.config)
+    kname = solver_kernel(args.rule)
+    traffic = profile_traffic(args.config, kname)
     line = {
         "metric": METRIC, "value": round(gteps, 3), "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
@@ -255,7 +261,7 @@ def run_ours(args, ws, rank, local):
                    "wall_s_timed_region": round(wall, 4)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "peak_source": peak_src, "kernel": "rounds_kernel (persistent)",
+                     "peak_source": peak_src, "kernel": f"{kname} (persistent)",
                      "bytes_alg_per_launch": bytes_alg},
         "e2e": {"value": round(ws * e_ref / (e2e_ms_step * 1e-3) / 1e9, 3), "unit": UNIT,
                 "ms_per_step": round(e2e_ms_step, 3),
@@ -357,7 +363,7 @@ def main():
     ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     ap.add_argument("--scale", type=int, default=0, help="override p0 (R-MAT scale / n / side)")
     ap.add_argument("--seed-offset", type=int, default=0)
-    ap.add_argument("--rule", type=int, default=2, help="0 reference, 1 snapshot, 2 auto")
+    ap.add_argument("--rule", type=int, default=2, help="0 reference, 1 counting, 2 auto (= counting)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -257,8 +257,8 @@ __device__ __forceinline__ void notify8(const CP<OffT, EstT>& p, const Enq& q, u
 // known to be >= lo, or only levels >= lo are asked for).  Returns (t,
 // count(>= t)), (cap, count(>= cap)) when nothing drops, or (0, deg) when no
 // level >= lo qualifies.
-template <bool RO, typename EstT>
-__device__ __noinline__ uint2 warp_window(const uint32_t* src, const EstT* snap,
+template <typename EstT>
+__device__ __forceinline__ uint2 warp_window(const uint32_t* src, bool ro, const EstT* snap,
                                           const EstT* s_cache, uint32_t cache_n, uint32_t* bins,
                                           uint64_t ob, uint64_t oe, uint32_t cap, uint32_t lo,
                                           uint32_t deg, bool fine_first) {
@@ -276,7 +276,7 @@ __device__ __noinline__ uint2 warp_window(const uint32_t* src, const EstT* snap,
     const uint32_t w = range > (uint32_t)WARP_BINS ? (range + WARP_BINS - 1) / WARP_BINS : 1u;
     warp_zero_bins(bins);
     uint32_t above = 0;
-    stream_row<32, RO>(src, snap, lane_id(), ob, oe, s_cache, cache_n,
+    stream_row_rt<32>(src, ro, snap, lane_id(), ob, oe, s_cache, cache_n,
                        [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
                          for (int k = 0; k < 8; ++k) {
@@ -307,8 +307,8 @@ __device__ __noinline__ uint2 warp_window(const uint32_t* src, const EstT* snap,
   }
 }
 
-template <bool RO, typename EstT>
-__device__ __noinline__ void cta_window(const uint32_t* src, const EstT* snap, const EstT* s_cache,
+template <typename EstT>
+__device__ __noinline__ void cta_window(const uint32_t* src, bool ro, const EstT* snap, const EstT* s_cache,
                                         uint32_t cache_n, uint32_t* s_hist, uint32_t* s_red,
                                         uint64_t ob, uint64_t oe, uint32_t cap, uint32_t lo,
                                         uint32_t deg, bool fine_first, uint32_t* out) {
@@ -328,7 +328,7 @@ __device__ __noinline__ void cta_window(const uint32_t* src, const EstT* snap, c
     for (int i = tid; i < HIST_BINS; i += SOLVE_THREADS) s_hist[i] = 0;
     __syncthreads();
     uint32_t above = 0;
-    stream_row<SOLVE_THREADS, RO>(src, snap, tid, ob, oe, s_cache, cache_n,
+    stream_row_rt<SOLVE_THREADS>(src, ro, snap, tid, ob, oe, s_cache, cache_n,
                                   [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
                                     for (int k = 0; k < 8; ++k) {
@@ -461,7 +461,7 @@ __device__ __forceinline__ void finish_eval(const CP<OffT, EstT>& p, const Item&
 }
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+__device__ __forceinline__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                           uint32_t* bins, const Item& it, Acc& acc) {
   if (it.spec) {
     if (lane_id() == 0) finish_eval(p, it, it.spec_t, it.spec_c, 0u, acc);
@@ -478,17 +478,17 @@ __device__ __noinline__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>
     }
     lo = cA;  // count(>= cA) >= count(>= cap) = cA: the answer is >= cA
   }
+  // pass 0: the list (levels >= max(lo, thr)); pass 1: the CSR row
   uint2 tc = make_uint2(0, 0);
   uint32_t scanned = 0;
-  if (it.list) {
-    tc = warp_window<false>(p.radj, snap, s_cache, cache_n, bins, it.ob, it.ob + it.len, it.cap,
-                            lo > it.thr ? lo : it.thr, it.deg, !v.r0);
-    scanned = it.len;
-  }
-  if (tc.x == 0) {  // no list, or the answer is below its threshold
-    tc = warp_window<true>(p.adj, snap, s_cache, cache_n, bins, it.ob, it.ob + it.deg, it.cap, lo,
-                           it.deg, !v.r0);
-    scanned += it.deg;
+#pragma unroll 1
+  for (int pass = it.list ? 0 : 1; pass < 2; ++pass) {
+    const bool lst = pass == 0;
+    const uint32_t len = lst ? it.len : it.deg;
+    tc = warp_window(lst ? (const uint32_t*)p.radj : p.adj, !lst, snap, s_cache, cache_n, bins,
+                     it.ob, it.ob + len, it.cap, lst && it.thr > lo ? it.thr : lo, it.deg, !v.r0);
+    scanned += len;
+    if (tc.x != 0) break;  // found (a list miss falls through to the row)
   }
   if (lane_id() == 0) finish_eval(p, it, tc.x, tc.y, scanned, acc);
 }
@@ -523,7 +523,7 @@ __device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>&
   }
   uint32_t scanned = 0;
   if (it.list) {
-    cta_window<false>(p.radj, snap, s_cache, cache_n, s_hist, sh.red, it.ob, it.ob + it.len,
+    cta_window(p.radj, false, snap, s_cache, cache_n, s_hist, sh.red, it.ob, it.ob + it.len,
                       it.cap, lo > it.thr ? lo : it.thr, it.deg, !v.r0, sh.out);
     scanned = it.len;
   } else if (threadIdx.x == 0) {
@@ -531,7 +531,7 @@ __device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>&
   }
   __syncthreads();
   if (sh.out[0] == 0) {
-    cta_window<true>(p.adj, snap, s_cache, cache_n, s_hist, sh.red, it.ob, it.ob + it.deg, it.cap,
+    cta_window(p.adj, true, snap, s_cache, cache_n, s_hist, sh.red, it.ob, it.ob + it.deg, it.cap,
                      lo, it.deg, !v.r0, sh.out);
     scanned += it.deg;
   }
@@ -911,10 +911,10 @@ __device__ __forceinline__ uint32_t list_threshold(uint32_t t) {
 
 // Returns the notifications fired by this lane (counted once per warp in
 // `acc` by the callers).
-template <bool RO, typename OffT, typename EstT>
-__device__ __noinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const Enq& q,
+template <typename OffT, typename EstT>
+__device__ __forceinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const Enq& q,
                                              const EstT* s_cache, uint32_t cache_n,
-                                             uint32_t* bins, const uint32_t* src, uint32_t u,
+                                             uint32_t* bins, const uint32_t* src, bool ro, uint32_t u,
                                              uint64_t ob, uint32_t len, uint32_t t, uint32_t cap,
                                              uint32_t build, uint32_t tag, uint32_t floor) {
   uint32_t cursor = 0;  // warp-uniform
@@ -923,7 +923,7 @@ __device__ __noinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const Enq&
   const uint32_t sl = t > (uint32_t)KC_SPEC_BINS ? t - KC_SPEC_BINS : 1u;
   const uint32_t slo = floor > sl ? floor : sl;  // spec window [slo, t)
   if (tag) warp_zero_bins(bins);
-  stream_row<32, RO>(src, p.N, lane_id(), ob, ob + len, s_cache, cache_n,
+  stream_row_rt<32>(src, ro, p.N, lane_id(), ob, ob + len, s_cache, cache_n,
                      [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
                        notify8(p, q, ok, ids, x, t, cap, fires);
                        if (tag) {
@@ -974,10 +974,10 @@ __device__ __noinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const Enq&
   return fires;
 }
 
-template <bool RO, typename OffT, typename EstT>
+template <typename OffT, typename EstT>
 __device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p, const Enq& q,
                                             const EstT* s_cache, uint32_t cache_n, Shared& sh,
-                                            uint32_t* s_hist, const uint32_t* src, uint32_t u,
+                                            uint32_t* s_hist, const uint32_t* src, bool ro, uint32_t u,
                                             uint64_t ob, uint32_t len, uint32_t t, uint32_t cap,
                                             uint32_t build, uint32_t tag, uint32_t floor) {
   const uint32_t tid = threadIdx.x;
@@ -988,7 +988,7 @@ __device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p, const Enq& 
     for (int i = tid; i < HIST_BINS; i += SOLVE_THREADS) s_hist[i] = 0;
   __syncthreads();
   uint32_t fires = 0, above = 0;
-  stream_row<SOLVE_THREADS, RO>(src, p.N, tid, ob, ob + len, s_cache, cache_n,
+  stream_row_rt<SOLVE_THREADS>(src, ro, p.N, tid, ob, ob + len, s_cache, cache_n,
                                 [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
                                   notify8(p, q, ok, ids, x, t, cap, fires);
                                   if (tag) {
@@ -1095,11 +1095,12 @@ __device__ __forceinline__ uint32_t notify_drop_warp(const CP<OffT, EstT>& p, co
                                                      uint32_t* bins, uint32_t round,
                                                      const Drop& d) {
   const uint32_t tag = KC_SPEC ? round + 1 : 0u;
-  if (d.thr)  // optionally in place: drop entries whose settled value fell below the threshold
-    return notify_warp<false>(p, q, s_cache, cache_n, bins, p.radj, d.u, d.ob, d.len, d.t, d.cap,
-                              KC_LIST_COMPACT ? d.thr : 0u, tag, d.thr);
-  return notify_warp<true>(p, q, s_cache, cache_n, bins, p.adj, d.u, d.ob, d.len, d.t, d.cap,
-                           list_build(round == 0, d), tag, 1u);
+  // a list (optionally filtered in place), or the CSR row (building the list)
+  const bool lst = d.thr != 0;
+  return notify_warp(p, q, s_cache, cache_n, bins, lst ? (const uint32_t*)p.radj : p.adj, !lst,
+                     d.u, d.ob, d.len, d.t, d.cap,
+                     lst ? (KC_LIST_COMPACT ? d.thr : 0u) : list_build(round == 0, d), tag,
+                     lst ? d.thr : 1u);
 }
 
 template <typename OffT, typename EstT>
@@ -1388,10 +1389,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     auto notify_long = [&](uint32_t u) {
       const Drop d = drop_item(p, u);  // a long-queued hub always dropped
       const uint32_t f =
-          d.thr ? notify_cta<false>(p, q, s_cache, cache_n, sh, s_hist, p.radj, d.u, d.ob, d.len,
-                                    d.t, d.cap, 0u, KC_SPEC ? r + 1 : 0u, d.thr)
-                : notify_cta<true>(p, q, s_cache, cache_n, sh, s_hist, p.adj, d.u, d.ob, d.len,
-                                   d.t, d.cap, list_build(v.r0, d), KC_SPEC ? r + 1 : 0u, 1u);
+          d.thr ? notify_cta(p, q, s_cache, cache_n, sh, s_hist, p.radj, false, d.u, d.ob, d.len,
+                             d.t, d.cap, 0u, KC_SPEC ? r + 1 : 0u, d.thr)
+                : notify_cta(p, q, s_cache, cache_n, sh, s_hist, p.adj, true, d.u, d.ob, d.len,
+                             d.t, d.cap, list_build(v.r0, d), KC_SPEC ? r + 1 : 0u, 1u);
       acc.fires += f;
       if (tid == 0) acc.nscan += d.len;
     };

@@ -296,6 +296,43 @@ __device__ __forceinline__ void stream_row(const uint32_t* src, const EstT* snap
   }
 }
 
+// Same stream with the load path chosen at run time (ro: immutable CSR rows
+// via the non-coherent path; else lists rewritten inside the kernel, L2
+// only) — one inlined copy serves both sources.
+__device__ __forceinline__ uint4 ld_ids4_rt(const uint32_t* src, uint64_t a, bool ro) {
+  return ro ? ld_ids4<true>(src, a) : ld_ids4<false>(src, a);
+}
+
+template <int NT, typename EstT, typename F>
+__device__ __forceinline__ void stream_row_rt(const uint32_t* src, bool ro, const EstT* snap,
+                                              uint32_t me, uint64_t ob, uint64_t oe,
+                                              const EstT* s_cache, uint32_t cache_n, F&& f) {
+  constexpr uint64_t STEP = (uint64_t)NT * 8;
+  uint64_t a = ob & ~(uint64_t)3;
+  uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
+  if (a + 4 * me < oe) q0 = ld_ids4_rt(src, a + 4 * me, ro);
+  if (a + 4 * me + 4 * NT < oe) q1 = ld_ids4_rt(src, a + 4 * me + 4 * NT, ro);
+  for (; a < oe; a += STEP) {
+    uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
+    const uint64_t nb = a + STEP;
+    if (nb + 4 * me < oe) n0 = ld_ids4_rt(src, nb + 4 * me, ro);
+    if (nb + 4 * me + 4 * NT < oe) n1 = ld_ids4_rt(src, nb + 4 * me + 4 * NT, ro);
+    uint32_t ids[8], x[8];
+    uint32_t ok = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint64_t pos = a + 4 * me + (k >> 2) * 4 * NT + (k & 3);
+      ids[k] = u4_get(k < 4 ? q0 : q1, k & 3);
+      const bool v = pos >= ob && pos < oe;
+      ok |= (uint32_t)v << k;
+      x[k] = v ? est_at(s_cache, cache_n, snap, ids[k]) : 0u;
+    }
+    f(ok, ids, x);
+    q0 = n0;
+    q1 = n1;
+  }
+}
+
 template <typename EstT>
 __device__ __forceinline__ void fill_cache(EstT* s_cache, const EstT* src, uint32_t cache_n) {
   // cache_n * sizeof(EstT) is a multiple of 16 bytes; 8 loads in flight per
