@@ -195,13 +195,35 @@ def make_configs(which):
             json.dump(have, f, indent=1)
 
 
+def add_ref_counters(which):
+    """RunReport of the unmodified reference kcore::fastk_run with its
+    defaults (batch 256, extended notify, hybrid tail) on the full-size
+    configs: the GPU's REFERENCE rule + hybrid tail must reproduce it."""
+    path = os.path.join(GOLDEN, "configs.json")
+    have = json.load(open(path))
+    for cfg in which:
+        n, pairs = gen(cfg)
+        g = O.build_csr(n, pairs)
+        del pairs
+        core, st = O.RefGraph(g).fastk(threads=8, batch=256, ext=True, hybrid=True)
+        assert sha(core.astype(np.uint32)) == have[str(cfg)]["coreness_sha256"]
+        have[str(cfg)]["reference_fastk_default"] = {k: int(st[k]) for k in (
+            "iterations", "messages_sent", "messages_drained", "tail_pops")}
+        print(cfg, have[str(cfg)]["reference_fastk_default"], flush=True)
+        with open(path, "w") as f:
+            json.dump(have, f, indent=1)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="", help="comma list of config ids to digest")
     ap.add_argument("--no-small", action="store_true")
+    ap.add_argument("--ref-counters", default="", help="comma list: add the reference's RunReport")
     a = ap.parse_args()
     O.build(ref=True)
     if not a.no_small:
         make_small()
     if a.configs:
         make_configs([int(x) for x in a.configs.split(",")])
+    if a.ref_counters:
+        add_ref_counters([int(x) for x in a.ref_counters.split(",")])

@@ -176,6 +176,7 @@ void free_solver(kc_graph* g) {
   dfree(g->sb.anydrop, g->stream);
   dfree(g->sb.stats, g->stream);
   dfree(g->sb.status, g->stream);
+  dfree(g->sb.tailc, g->stream);
   dfree(g->d_out, g->stream);
   dfree(g->d_k, g->stream);
   dfree(g->d_prof, g->stream);
@@ -224,6 +225,7 @@ kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
   CK(dmalloc((void**)&b.anydrop, 4 * sizeof(uint32_t), g->stream));
   CK(dmalloc((void**)&b.stats, (size_t)STAT_SLOTS * sizeof(RoundStat), g->stream));
   CK(dmalloc((void**)&b.status, 4 * sizeof(uint32_t), g->stream));
+  CK(dmalloc((void**)&b.tailc, TAIL_SLOTS * sizeof(unsigned long long), g->stream));
   CK(dmalloc((void**)&g->d_out, (g->n ? g->n : 1) * sizeof(uint32_t), g->stream));
   CK(dmalloc((void**)&g->d_k, 2 * sizeof(unsigned long long), g->stream));
   CK(dmalloc((void**)&g->d_count, sizeof(unsigned long long), g->stream));
@@ -250,6 +252,11 @@ kc_status validate(const kc_options* opt, kc_options* o) {
   return KC_OK;
 }
 
+// The reference rule with hybrid_tail finishes like fastk_run: once fewer
+// than `batch` vertices are active, the sequential tail (kc_tail.cu).  The
+// counting rule has no use for it (its rounds only hold droppers).
+bool uses_tail(const kc_options& o) { return o.hybrid_tail && map_rule(o) != R_COUNT; }
+
 // The counting rule runs on kc_count.cu's solver (lists + direct queues)
 // unless the legacy flag-frontier solver is requested for A/B runs.
 bool uses_count_kernel(const kc_options& o) {
@@ -270,7 +277,8 @@ uint32_t cache_entries(const kc_graph* g, const kc_options& o) {
 
 // Run the solver to convergence (or one round when `one_round`), leaving the
 // estimates on the device.  Fills the counters of `st`.
-kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_t r_end) {
+kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_t r_end,
+                     bool tail_switch) {
   if ((o.reserved[0] & KC_DEBUG_PHASE_TIMES) && !g->d_prof) {
     CK(dmalloc((void**)&g->d_prof, (size_t)PROF_ROUNDS * g->num_sms * PROF_PHASES * 8, g->stream));
     CK(cudaMemsetAsync(g->d_prof, 0, (size_t)PROF_ROUNDS * g->num_sms * PROF_PHASES * 8, g->stream));
@@ -281,7 +289,7 @@ kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_
   c.clamp_drop = g->lay.max_degree > g->lay.h_graph ? 1u : 0u;
   c.cache_n = cache_entries(g, o);
   c.max_rounds = o.max_rounds;
-  c.tail_threshold = 0;
+  c.tail_threshold = tail_switch ? o.batch : 0u;
   c.num_sms = g->num_sms;
   if (uses_count_kernel(o))
     CK(launch_count_rounds(g->sb, c, g->est16, g->lay.off64, r_begin, r_end, g->stream));
@@ -291,6 +299,7 @@ kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_
 }
 
 kc_status init_state(kc_graph* g, const kc_options& o) {
+  CK(cudaMemsetAsync(g->sb.tailc, 0, TAIL_SLOTS * sizeof(unsigned long long), g->stream));
   if (uses_count_kernel(o))
     CK(launch_count_init(g->sb, g->est16, g->lay.off64, g->lay.h_graph, g->stream));
   else
@@ -322,8 +331,18 @@ kc_status collect(kc_graph* g, const kc_options& o, kc_stats* st, bool* converge
   // (fastk.cpp:128-149 sweeps all ids); they cost nothing here.
   st->messages_drained = st->v_eval + (rounds ? (uint64_t)(g->n - g->lay.n_nz) : 0);
   st->tail_pops = 0;
-  st->tail_rounds = status[2];
-  (void)o;
+  st->tail_rounds = 0;
+  if (uses_tail(o)) {  // fastk.cpp:175-185: the tail's pops, evaluations, notifications
+    unsigned long long tc[TAIL_SLOTS];
+    CK(cudaMemcpy(tc, g->sb.tailc, sizeof(tc), cudaMemcpyDeviceToHost));
+    st->tail_pops = tc[TAIL_POPS];
+    st->messages_sent += tc[TAIL_FIRES];
+    st->v_eval += tc[TAIL_EVALS];
+    st->messages_drained += tc[TAIL_EVALS];
+    st->e_scan += tc[TAIL_ESCAN];
+    st->drops += tc[TAIL_DROPS];
+    st->tail_rounds = tc[TAIL_RAN];
+  }
   return KC_OK;
 }
 
@@ -536,8 +555,11 @@ static kc_status solve_impl(kc_graph* g, const kc_options* opt, uint32_t* out, b
   CK(cudaEventRecord(g->ev[0], g->stream));
   s = init_state(g, o);
   if (s != KC_OK) return s;
-  s = run_rounds(g, o, 0, o.max_rounds);
+  s = run_rounds(g, o, 0, o.max_rounds, uses_tail(o));
   if (s != KC_OK) return s;
+  if (uses_tail(o))  // a no-op unless the rounds stopped for the tail
+    CK(launch_tail(g->sb, g->lay.perm, g->est16, g->lay.off64, o.extended_notify != 0, -1,
+                   g->num_sms, g->stream));
   CK(cudaEventRecord(g->ev[1], g->stream));
   bool conv = false;
   s = collect(g, o, st, &conv);
@@ -611,7 +633,7 @@ kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn 
   if (fn && fn(user, 0, snap.data(), g->n, g->n)) return fail(KC_ERR_CALLBACK, "inspector");
   bool conv = false;
   for (uint32_t r = 0; r < o.max_rounds && !conv; ++r) {
-    s = run_rounds(g, o, r, r + 1);
+    s = run_rounds(g, o, r, r + 1, false);
     if (s != KC_OK) return s;
     s = collect(g, o, nullptr, &conv);
     if (s != KC_OK) return s;
@@ -635,6 +657,21 @@ kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn 
     CK(cudaStreamSynchronize(g->stream));
     if (fn && fn(user, (uint64_t)r + 1, snap.data(), g->n, active))
       return fail(KC_ERR_CALLBACK, "inspector");
+    if (!conv && uses_tail(o) && active < o.batch) {
+      // hybrid switch after round r (fastk.cpp:113-115): the sequential tail
+      // from round r+1's active flags, then one more boundary with nothing
+      // active (fastk.cpp:180-183)
+      CK(launch_tail(g->sb, g->lay.perm, g->est16, g->lay.off64, o.extended_notify != 0,
+                     (int)((r + 1) & 1), g->num_sms, g->stream));
+      s = permute_back(g);
+      if (s != KC_OK) return s;
+      CK(cudaMemcpyAsync(snap.data(), g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                         g->stream));
+      CK(cudaStreamSynchronize(g->stream));
+      if (fn && fn(user, (uint64_t)r + 2, snap.data(), g->n, 0))
+        return fail(KC_ERR_CALLBACK, "inspector");
+      conv = true;
+    }
   }
   if (!conv) return fail(KC_ERR_NOT_CONVERGED, "round cap reached");
   s = collect(g, o, st, &conv);

@@ -81,6 +81,9 @@ constexpr int WQ = 64;             // per-warp, per-class enqueue buffer (flushe
 #ifndef KC_LIST_COMPACT
 #define KC_LIST_COMPACT 0          // 1: notify filters lists in place (warp scans)
 #endif
+#ifndef KC_R0_LISTS
+#define KC_R0_LISTS 0              // 1: round-0 droppers build their lists in round 0's notify
+#endif
 #ifndef KC_LIST_SHIFT
 #define KC_LIST_SHIFT 1            // list threshold L = t - (t >> KC_LIST_SHIFT)
 #endif
@@ -1086,7 +1089,7 @@ __device__ __forceinline__ Drop drop_item(const CP<OffT, EstT>& p, uint32_t u) {
 }
 
 __device__ __forceinline__ uint32_t list_build(bool r0, const Drop& d) {
-  return (!r0 && d.deg > LIST_MIN_DEG) ? list_threshold(d.t) : 0u;
+  return ((KC_R0_LISTS || !r0) && d.deg > LIST_MIN_DEG) ? list_threshold(d.t) : 0u;
 }
 
 template <typename OffT, typename EstT>

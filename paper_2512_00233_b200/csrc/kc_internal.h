@@ -75,10 +75,15 @@ struct SolveBuffers {
   Ctl* ctl;                  // [2]
   uint32_t* anydrop;         // [3] "some estimate dropped in round r" (r % 3)
   RoundStat* stats;          // [STAT_SLOTS]
-  uint32_t* status;          // [0] rounds completed, [1] converged, [2] tail rounds,
+  uint32_t* status;          // [0] rounds completed, [1] converged, [2] stopped for the tail,
                              // [3] est buffer holding the current state
   unsigned long long* prof;  // optional phase timestamps [PROF_ROUNDS][grid][PROF_PHASES]
+  unsigned long long* tailc; // hybrid tail (kc_tail.cu): counters [TAIL_SLOTS]
 };
+// kc_tail.cu counters (tailc[]): pops (tail_pops), evaluations, notifications,
+// drops, adjacency entries scanned, "the tail ran"; slot 6 is scratch.
+enum TailSlot : int { TAIL_POPS = 0, TAIL_EVALS, TAIL_FIRES, TAIL_DROPS, TAIL_ESCAN, TAIL_RAN,
+                      TAIL_SCRATCH, TAIL_SLOTS = 8 };
 constexpr uint32_t PROF_ROUNDS = 256;
 constexpr uint32_t PROF_PHASES = 8;
 
@@ -87,7 +92,9 @@ struct SolveConfig {
   uint32_t clamp_drop;       // max degree > H (round 0 changed in the reference)
   uint32_t cache_n;          // ids cached in shared memory
   uint32_t max_rounds;
-  uint32_t tail_threshold;   // frontier size below which one CTA finishes (0 = off)
+  uint32_t tail_threshold;   // reference rule + hybrid_tail: stop the rounds when a round
+                             // starts with fewer active vertices (the batch, fastk.hpp:29-31)
+                             // and leave the rest to the sequential tail (0 = off)
   int num_sms;
 };
 
@@ -98,6 +105,11 @@ cudaError_t launch_rounds(const SolveBuffers& b, const SolveConfig& c, bool est1
 // The counting-rule solver (kc_count.cu): same contract.
 cudaError_t launch_count_rounds(const SolveBuffers& b, const SolveConfig& c, bool est16, bool off64,
                                 uint32_t r_begin, uint32_t r_end, cudaStream_t stream);
+// FastK's sequential tail (fastk.cpp:28-55) on one CTA, after the rounds
+// kernel stopped for it (status[2] == 1) — or, with force_flags >= 0, from
+// the active set in flag[force_flags] (observed mode).  No-op otherwise.
+cudaError_t launch_tail(const SolveBuffers& b, const uint32_t* perm, bool est16, bool off64,
+                        int ext, int force_flags, int num_sms, cudaStream_t s);
 cudaError_t launch_count_init(const SolveBuffers& b, bool est16, bool off64, uint32_t h_graph,
                               cudaStream_t stream);
 // Initialise estimates (min(deg, H)), round-0 frontier, counters.

@@ -70,6 +70,7 @@ struct P {
   int rule;
   uint32_t cache_n;
   uint32_t clamp_drop;  // max degree > H: the reference's round 0 lowers deg -> <= H
+  uint32_t tail_batch;  // hybrid_tail: switch threshold (0 = off)
 };
 
 // Per-round view: what this round reads and writes.
@@ -648,6 +649,25 @@ __global__ void __launch_bounds__(SOLVE_THREADS, KC_CTAS_PER_SM) rounds_kernel(P
     uint32_t active = 0;
 #pragma unroll
     for (int c = 0; c < NCLS; ++c) active += rv.qcnt[c];
+    if (r >= 1 && active < p.tail_batch) {
+      // hybrid switch (fastk.cpp:113-115, switch_condition fastk.hpp:29-31):
+      // round r-1 changed something and fewer than `batch` vertices are
+      // active — stop here, leave round r's active set in flag[cur] for the
+      // sequential tail (kc_tail.cu).  Grid-uniform: every CTA read the
+      // same class sizes after the grid sync.
+      for (int c = 0; c < NCLS; ++c)
+        for (uint32_t i = blockIdx.x * SOLVE_THREADS + tid; i < rv.qcnt[c];
+             i += gridDim.x * SOLVE_THREADS)
+          p.flag[cur][p.queue[p.cb[c] + i]] = 1;
+      if (blockIdx.x == 0 && tid == 0) {
+        p.status[0] = r;  // rounds executed (rep.iterations at the switch)
+        p.status[1] = 1;
+        p.status[2] = 1;
+        p.status[3] = 0;
+      }
+      if (pf) pf[1] = pf[2] = pf[3] = pf[4] = pf[5] = pf[6] = pf[7] = gtimer();
+      return;
+    }
     const uint32_t cache_n = active >= CACHE_MIN_ACTIVE ? p.cache_n : 0u;
     if (blockIdx.x == 0 && tid == 0) {
       p.stats[sr].q01 = rv.qcnt[0] | (unsigned long long)rv.qcnt[1] << 32;
@@ -772,6 +792,7 @@ cudaError_t launch_rounds_t(const SolveBuffers& b, const SolveConfig& c, uint32_
   p.rule = c.rule;
   p.cache_n = c.cache_n;
   p.clamp_drop = c.clamp_drop;
+  p.tail_batch = c.tail_threshold;
   const size_t warp_region = (size_t)NWARPS * WARP_BINS;
   const size_t hist = (size_t)HIST_BINS > warp_region ? (size_t)HIST_BINS : warp_region;
   const size_t smem = (((size_t)c.cache_n * sizeof(EstT) + 15) & ~(size_t)15) +

@@ -309,6 +309,11 @@ def test_full_size_configs_vs_golden(gpu, cfg):
         assert st2["iterations"] == j["iterations"]
         assert st2["messages_sent"] == j["messages_sent"]
         assert st2["e_scan"] == j["e_scan"]
+    if "reference_fastk_default" in d:  # the reference's defaults incl. the hybrid tail
+        core3, st3 = gg.solve(gpu.FastKOptions(rule=gpu.Rule.REFERENCE))
+        assert np.array_equal(core, core3)
+        want = d["reference_fastk_default"]
+        assert {k: st3[k] for k in want} == want
 
 
 def test_invalid_arguments_on_device(gpu):
