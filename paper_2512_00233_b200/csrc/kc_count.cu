@@ -858,39 +858,101 @@ __device__ __noinline__ void eval_sub(const CP<OffT, EstT>& p, const View<EstT>&
 }
 
 // THREAD class (deg <= 8): thread per vertex, h = max_i min(x_i, #{x_j >= x_i}).
+// A warp grabs up to GMAX_THREAD ids per atomic and each lane works TU
+// vertices at a time, their loads issued level by level (offsets, ids,
+// gathers) so that one lane keeps up to 8 * TU gathers in flight: a round
+// of millions of degree-3 vertices (the road-like grid) is bound by memory
+// parallelism, not by per-vertex latency or by the shared grab cursor.
+#ifndef KC_TU
+#define KC_TU 2
+#endif
+constexpr int TU = KC_TU;                       // evaluate: vertices per lane per pass
+constexpr int TUN = 2;                          // notify: droppers per lane per pass
+constexpr uint32_t GMAX_THREAD = 32u * TU * 4u;  // ids per grab (max)
+
+__device__ __forceinline__ uint32_t warp_grab(uint32_t* cursor, uint32_t cnt, uint32_t G) {
+  uint32_t base = 0;
+  if (lane_id() == 0)  // plain read first: no atomic once the queue is drained
+    base = *reinterpret_cast<volatile uint32_t*>(cursor) >= cnt ? cnt : atomicAdd(cursor, G);
+  return __shfl_sync(FULL, base, 0);
+}
+
+// Lane-level walk of class c's queue: proc(u[K], valid mask) per pass.
+template <int K, typename OffT, typename EstT, typename F>
+__device__ __forceinline__ void for_class_lanes(const CP<OffT, EstT>& p, const View<EstT>& v, int c,
+                                                uint32_t gmax, F&& proc) {
+  const uint32_t cnt = v.qcnt[c];
+  if (cnt == 0) return;
+  const uint32_t G = grab_size(cnt, gmax);
+  const uint32_t lane = lane_id();
+  for (;;) {
+    const uint32_t base = warp_grab(&v.grab[c], cnt, G);
+    if (base >= cnt) break;
+    const uint32_t n = cnt - base < G ? cnt - base : G;
+    for (uint32_t s0 = 0; s0 < n; s0 += 32u * K) {
+      uint32_t u[K], valid = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t i = s0 + lane + 32u * k;
+        u[k] = 0;
+        if (i < n) {
+          u[k] = v.q ? v.q[p.cb[c] + base + i] : p.cb[c] + base + i;
+          valid |= 1u << k;
+        }
+      }
+      proc(u, valid);
+    }
+  }
+}
+
 template <typename OffT, typename EstT>
 __device__ __noinline__ void eval_thread(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                             Acc& acc) {
   constexpr int R = DEG_THREAD_MAX;
   const EstT* snap = v.snap;
   const uint32_t cache_n = v.cache_n;
-  for_class(p, v, C_THREAD, GMAX_SMALL, [&](uint32_t u, uint32_t n) {
-    if (lane_id() >= n) return;
-    const uint64_t ob = p.off[u];
-    const uint32_t deg = (uint32_t)(p.off[u + 1] - ob);
-    const uint32_t cap = est_at(s_cache, cache_n, snap, u);
-    uint32_t x[R];
+  for_class_lanes<TU>(p, v, C_THREAD, GMAX_THREAD, [&](const uint32_t(&u)[TU], uint32_t valid) {
+    uint64_t ob[TU];
+    uint32_t deg[TU], cap[TU], x[TU][R];
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const uint32_t id = (uint32_t)j < deg ? p.adj[ob + j] : 0xffffffffu;
-      x[j] = id != 0xffffffffu ? est_at(s_cache, cache_n, snap, id) : 0u;
+    for (int k = 0; k < TU; ++k) {
+      ob[k] = 0;
+      deg[k] = cap[k] = 0;
+      if (valid >> k & 1) {
+        ob[k] = p.off[u[k]];
+        deg[k] = (uint32_t)(p.off[u[k] + 1] - ob[k]);
+        cap[k] = est_at(s_cache, cache_n, snap, u[k]);
+      }
     }
-    uint32_t h = 0;
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
+    for (int k = 0; k < TU; ++k)
+#pragma unroll
+      for (int j = 0; j < R; ++j) x[k][j] = (uint32_t)j < deg[k] ? p.adj[ob[k] + j] : 0xffffffffu;
+#pragma unroll
+    for (int k = 0; k < TU; ++k)
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        x[k][j] = x[k][j] != 0xffffffffu ? est_at(s_cache, cache_n, snap, x[k][j]) : 0u;
+#pragma unroll
+    for (int k = 0; k < TU; ++k) {
+      if (!(valid >> k & 1)) continue;
+      uint32_t h = 0;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int j = 0; j < R; ++j) c += x[k][j] >= x[k][i];
+        const uint32_t m = x[k][i] < c ? x[k][i] : c;
+        h = m > h ? m : h;
+      }
+      const uint32_t t = h < cap[k] ? h : cap[k];
       uint32_t c = 0;
 #pragma unroll
-      for (int j = 0; j < R; ++j) c += x[j] >= x[i];
-      const uint32_t m = x[i] < c ? x[i] : c;
-      h = m > h ? m : h;
+      for (int j = 0; j < R; ++j) c += x[k][j] >= t;
+      Item it;
+      it.u = u[k]; it.cap = cap[k]; it.deg = deg[k]; it.len = deg[k]; it.thr = 0;
+      finish_eval(p, it, t, t ? c : deg[k], deg[k], acc);
     }
-    const uint32_t t = h < cap ? h : cap;
-    uint32_t c = 0;
-#pragma unroll
-    for (int j = 0; j < R; ++j) c += x[j] >= t;
-    Item it;
-    it.u = u; it.cap = cap; it.deg = deg; it.len = deg; it.thr = 0;
-    finish_eval(p, it, t, t ? c : deg, deg, acc);
   });
 }
 
@@ -1247,6 +1309,76 @@ __device__ __noinline__ void notify_small(const CP<OffT, EstT>& p, const View<Es
   acc.nscan += nscan;
 }
 
+// THREAD droppers: lane per dropper, TUN droppers per lane per pass, loads
+// issued level by level (estimates, offsets, ids, gathers, counters).
+template <typename OffT, typename EstT>
+__device__ __noinline__ void notify_thread(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                           const Enq& q, const EstT* s_cache, Acc& acc) {
+  constexpr int R = DEG_THREAD_MAX;
+  const uint32_t cache_n = v.cache_n;
+  uint32_t fires = 0, nscan = 0;
+  for_class_lanes<TUN>(p, v, C_THREAD, GMAX_THREAD, [&](const uint32_t(&u)[TUN], uint32_t valid) {
+    uint32_t t[TUN], cap[TUN], deg[TUN], ids[TUN][R], x[TUN][R];
+    uint64_t ob[TUN];
+    // estimates and offsets in one level (offsets of non-droppers are
+    // loaded for nothing: cheaper than another dependent round trip)
+#pragma unroll
+    for (int k = 0; k < TUN; ++k) {
+      t[k] = cap[k] = 0;
+      ob[k] = 0;
+      deg[k] = 0;
+      if (valid >> k & 1) {
+        t[k] = p.N[u[k]];
+        cap[k] = p.E[u[k]];
+        ob[k] = p.off[u[k]];
+        deg[k] = (uint32_t)(p.off[u[k] + 1] - ob[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < TUN; ++k)
+      if (!(t[k] < cap[k])) deg[k] = 0;  // not dropped this round
+#pragma unroll
+    for (int k = 0; k < TUN; ++k)
+#pragma unroll
+      for (int j = 0; j < R; ++j) ids[k][j] = (uint32_t)j < deg[k] ? p.adj[ob[k] + j] : 0u;
+#pragma unroll
+    for (int k = 0; k < TUN; ++k)
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        x[k][j] = (uint32_t)j < deg[k] ? est_at(s_cache, cache_n, (const EstT*)p.N, ids[k][j]) : 0u;
+    // should_notify(t, cap, N[w]) (fastk.hpp:25-27) == the drop removes u
+    // from w's support count; the decrement that crosses N[w] activates w
+    uint32_t act[TUN];
+#pragma unroll
+    for (int k = 0; k < TUN; ++k) {
+      uint32_t fire = 0;
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        fire |= (uint32_t)((uint32_t)j < deg[k] && t[k] < x[k][j] && x[k][j] <= cap[k]) << j;
+      fires += __popc(fire);
+      uint32_t old[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) old[j] = (fire >> j & 1) ? atomicSub(&p.cnt[ids[k][j]], 1u) : 0u;
+      act[k] = 0;
+#pragma unroll
+      for (int j = 0; j < R; ++j) act[k] |= (uint32_t)((fire >> j & 1) && old[j] == x[k][j]) << j;
+      if (t[k] < cap[k]) {
+        nscan += deg[k];
+        p.E[u[k]] = (EstT)t[k];  // apply (fastk.cpp:153)
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < TUN; ++k)
+      if (__any_sync(FULL, act[k])) {
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          if (__any_sync(FULL, act[k] >> j & 1)) wq_push(p, q, (act[k] >> j & 1) != 0, ids[k][j]);
+      }
+  });
+  acc.fires += fires;
+  acc.nscan += nscan;
+}
+
 template <typename OffT, typename EstT>
 __device__ __forceinline__ void flush_acc(const CP<OffT, EstT>& p, uint32_t sr, const Acc& acc,
                                           unsigned long long* s_acc) {
@@ -1421,7 +1553,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
       flat_notify(p, v, q, s_cache, w_bins, s_flat[warp_id()], C_WARP, GMAX_WARP, acc);
     }
     notify_small(p, v, q, s_cache, C_SUB, acc);
-    notify_small(p, v, q, s_cache, C_THREAD, acc);
+    notify_thread(p, v, q, s_cache, acc);
     consume_long(p, v, sh, ctl, 1, true, notify_long);
 #pragma unroll 1
     for (int c = 0; c < NCLS; ++c) wq_flush(p, q, c);

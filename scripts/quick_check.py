@@ -13,7 +13,7 @@ def check(name, n, pairs, rules=(K.Rule.COUNTING, K.Rule.REFERENCE)):
     for rule in rules:
         for ext in (True, False):
             t = time.time()
-            core, st = gg.solve(K.FastKOptions(rule=rule, extended_notify=ext))
+            core, st = gg.solve(K.FastKOptions(rule=rule, extended_notify=ext, hybrid_tail=False))
             ok = np.array_equal(core, truth)
             j = O.jacobi(g, "ref_ext" if ext else "ref_plain")
             extra = ""

@@ -229,9 +229,13 @@ def test_long_path_many_rounds(gpu):
     n = 3001
     G = gpu.Graph.from_edges(n, [(i, i + 1) for i in range(n - 1)])
     for rule in RULES:
-        core, r = solve(gpu, G, rule)
+        core, r = solve(gpu, G, rule, hybrid_tail=False)
         assert (core == 1).all()
         assert r.report.iterations >= n // 2 - 2
+    # with the reference's hybrid tail the chain is finished by the tail
+    # right after round 0 (2 vertices active < batch)
+    core, r = solve(gpu, G, "REFERENCE")
+    assert (core == 1).all() and r.report.iterations == 1 and r.report.tail_pops > 0
 
 
 # ---------------------------------------------------------------- layouts
