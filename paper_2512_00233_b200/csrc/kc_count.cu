@@ -131,6 +131,21 @@ struct Acc {  // per-thread counters, flushed per round
   bool any_drop;
 };
 
+struct Acc32 {  // the same, per phase call, in registers (32-bit: one phase's share)
+  uint32_t evals, escan, drops, fires, nscan, ascan;
+  bool any_drop;
+};
+
+__device__ __forceinline__ void merge_acc(Acc& to, const Acc32& a) {
+  to.evals += a.evals;
+  to.escan += a.escan;
+  to.drops += a.drops;
+  to.fires += a.fires;
+  to.nscan += a.nscan;
+  to.ascan += a.ascan;
+  to.any_drop |= a.any_drop;
+}
+
 struct Shared {  // per-CTA bookkeeping (static shared memory)
   uint32_t red[33];
   uint32_t item;
@@ -446,9 +461,9 @@ __device__ __forceinline__ Item eval_item(const CP<OffT, EstT>& p, const View<Es
   return it;
 }
 
-template <typename OffT, typename EstT>
+template <typename OffT, typename EstT, typename A>
 __device__ __forceinline__ void finish_eval(const CP<OffT, EstT>& p, const Item& it, uint32_t t,
-                                            uint32_t c, uint32_t scanned, Acc& acc) {
+                                            uint32_t c, uint32_t scanned, A& acc) {
   acc.evals += 1;
   acc.escan += it.deg;
   acc.ascan += scanned;
@@ -463,9 +478,9 @@ __device__ __forceinline__ void finish_eval(const CP<OffT, EstT>& p, const Item&
   if (it.thr != 0 && t < it.thr) p.rthr[it.u] = 0;
 }
 
-template <typename OffT, typename EstT>
+template <typename OffT, typename EstT, typename A>
 __device__ __forceinline__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
-                          uint32_t* bins, const Item& it, Acc& acc) {
+                          uint32_t* bins, const Item& it, A& acc) {
   if (it.spec) {
     if (lane_id() == 0) finish_eval(p, it, it.spec_t, it.spec_c, 0u, acc);
     return;
@@ -618,9 +633,9 @@ __device__ void consume_long(const CP<OffT, EstT>& p, const View<EstT>& v, Share
 
 // WARP and BIG classes: warp per vertex; metadata of a grab loaded one lane
 // per item, then walked.
-template <typename OffT, typename EstT>
-__device__ __noinline__ void eval_wclass(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
-                            uint32_t* bins, int c, uint32_t gmax, Acc& acc) {
+template <typename OffT, typename EstT, typename A>
+__device__ __forceinline__ void eval_wclass_impl(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                            uint32_t* bins, int c, uint32_t gmax, A& acc) {
   for_class(p, v, c, gmax, [&](uint32_t u, uint32_t n) {
     Item mine{};
     if (lane_id() < n) mine = eval_item(p, v, s_cache, u);
@@ -640,6 +655,16 @@ __device__ __noinline__ void eval_wclass(const CP<OffT, EstT>& p, const View<Est
       eval_warp(p, v, s_cache, bins, it, acc);
     }
   });
+}
+
+// Counters in registers for the whole phase (an Acc& into the kernel's
+// frame would be local-memory traffic per evaluation).
+template <typename OffT, typename EstT>
+__device__ __noinline__ void eval_wclass(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                            uint32_t* bins, int c, uint32_t gmax, Acc& acc) {
+  Acc32 a{0, 0, 0, 0, 0, 0, false};
+  eval_wclass_impl(p, v, s_cache, bins, c, gmax, a);
+  merge_acc(acc, a);
 }
 
 // ------------------------------------------------------------------------
@@ -713,10 +738,10 @@ __device__ __forceinline__ void flat_stream(const CP<OffT, EstT>& p, const FlatW
   }
 }
 
-template <typename OffT, typename EstT>
-__device__ __noinline__ void flat_eval(const CP<OffT, EstT>& p, const View<EstT>& v,
+template <typename OffT, typename EstT, typename A>
+__device__ __forceinline__ void flat_eval_impl(const CP<OffT, EstT>& p, const View<EstT>& v,
                                        const EstT* s_cache, uint32_t* bins, FlatW& fw, int c,
-                                       uint32_t gmax, Acc& acc) {
+                                       uint32_t gmax, A& acc) {
   const uint32_t lane = lane_id();
   const EstT* snap = v.snap;
   const uint32_t cache_n = v.cache_n;
@@ -792,11 +817,20 @@ __device__ __noinline__ void flat_eval(const CP<OffT, EstT>& p, const View<EstT>
   });
 }
 
+template <typename OffT, typename EstT>
+__device__ __noinline__ void flat_eval(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                       const EstT* s_cache, uint32_t* bins, FlatW& fw, int c,
+                                       uint32_t gmax, Acc& acc) {
+  Acc32 a{0, 0, 0, 0, 0, 0, false};
+  flat_eval_impl(p, v, s_cache, bins, fw, c, gmax, a);
+  merge_acc(acc, a);
+}
+
 // SUB class (deg <= 64): 8-lane tile per vertex, 8 values per lane,
 // bisection on [lo, cap).
-template <typename OffT, typename EstT>
-__device__ __noinline__ void eval_sub(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
-                         Acc& acc) {
+template <typename OffT, typename EstT, typename A>
+__device__ __forceinline__ void eval_sub_impl(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                         A& acc) {
   constexpr int R = DEG_SUB_MAX / 8;
   const uint32_t g = lane_id() >> 3, k = lane_id() & 7;
   const EstT* snap = v.snap;
@@ -857,6 +891,14 @@ __device__ __noinline__ void eval_sub(const CP<OffT, EstT>& p, const View<EstT>&
   });
 }
 
+template <typename OffT, typename EstT>
+__device__ __noinline__ void eval_sub(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                         Acc& acc) {
+  Acc32 a{0, 0, 0, 0, 0, 0, false};
+  eval_sub_impl(p, v, s_cache, a);
+  merge_acc(acc, a);
+}
+
 // THREAD class (deg <= 8): thread per vertex, h = max_i min(x_i, #{x_j >= x_i}).
 // A warp grabs up to GMAX_THREAD ids per atomic and each lane works TU
 // vertices at a time, their loads issued level by level (offsets, ids,
@@ -905,9 +947,9 @@ __device__ __forceinline__ void for_class_lanes(const CP<OffT, EstT>& p, const V
   }
 }
 
-template <typename OffT, typename EstT>
-__device__ __noinline__ void eval_thread(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
-                            Acc& acc) {
+template <typename OffT, typename EstT, typename A>
+__device__ __forceinline__ void eval_thread_impl(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                            A& acc) {
   constexpr int R = DEG_THREAD_MAX;
   const EstT* snap = v.snap;
   const uint32_t cache_n = v.cache_n;
@@ -954,6 +996,14 @@ __device__ __noinline__ void eval_thread(const CP<OffT, EstT>& p, const View<Est
       finish_eval(p, it, t, t ? c : deg[k], deg[k], acc);
     }
   });
+}
+
+template <typename OffT, typename EstT>
+__device__ __noinline__ void eval_thread(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+                            Acc& acc) {
+  Acc32 a{0, 0, 0, 0, 0, 0, false};
+  eval_thread_impl(p, v, s_cache, a);
+  merge_acc(acc, a);
 }
 
 // ------------------------------------------------------------------------
@@ -1168,10 +1218,10 @@ __device__ __forceinline__ uint32_t notify_drop_warp(const CP<OffT, EstT>& p, co
                      lst ? d.thr : 1u);
 }
 
-template <typename OffT, typename EstT>
-__device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p, const View<EstT>& v,
+template <typename OffT, typename EstT, typename A>
+__device__ __forceinline__ void notify_wclass_impl(const CP<OffT, EstT>& p, const View<EstT>& v,
                                            const Enq& q, const EstT* s_cache, uint32_t* bins,
-                                           int c, uint32_t gmax, Acc& acc) {
+                                           int c, uint32_t gmax, A& acc) {
   const uint32_t cache_n = v.cache_n;
   const bool r0 = v.r0;
   uint32_t fires = 0;
@@ -1198,9 +1248,18 @@ __device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p, const View<E
 }
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ void flat_notify(const CP<OffT, EstT>& p, const View<EstT>& v,
+__device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                           const Enq& q, const EstT* s_cache, uint32_t* bins,
+                                           int c, uint32_t gmax, Acc& acc) {
+  Acc32 a{0, 0, 0, 0, 0, 0, false};
+  notify_wclass_impl(p, v, q, s_cache, bins, c, gmax, a);
+  merge_acc(acc, a);
+}
+
+template <typename OffT, typename EstT, typename A>
+__device__ __forceinline__ void flat_notify_impl(const CP<OffT, EstT>& p, const View<EstT>& v,
                                          const Enq& q, const EstT* s_cache, uint32_t* bins,
-                                         FlatW& fw, int c, uint32_t gmax, Acc& acc) {
+                                         FlatW& fw, int c, uint32_t gmax, A& acc) {
   const uint32_t lane = lane_id();
   const uint32_t cache_n = v.cache_n;
   uint32_t fires = 0, nscan = 0;
@@ -1268,10 +1327,19 @@ __device__ __noinline__ void flat_notify(const CP<OffT, EstT>& p, const View<Est
   acc.nscan += nscan;
 }
 
-// SUB and THREAD droppers: 8-lane tile per dropper, up to 8 neighbours per lane.
 template <typename OffT, typename EstT>
-__device__ __noinline__ void notify_small(const CP<OffT, EstT>& p, const View<EstT>& v,
-                                          const Enq& q, const EstT* s_cache, int c, Acc& acc) {
+__device__ __noinline__ void flat_notify(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                         const Enq& q, const EstT* s_cache, uint32_t* bins,
+                                         FlatW& fw, int c, uint32_t gmax, Acc& acc) {
+  Acc32 a{0, 0, 0, 0, 0, 0, false};
+  flat_notify_impl(p, v, q, s_cache, bins, fw, c, gmax, a);
+  merge_acc(acc, a);
+}
+
+// SUB and THREAD droppers: 8-lane tile per dropper, up to 8 neighbours per lane.
+template <typename OffT, typename EstT, typename A>
+__device__ __forceinline__ void notify_small_impl(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                          const Enq& q, const EstT* s_cache, int c, A& acc) {
   const uint32_t g = lane_id() >> 3, k = lane_id() & 7;
   const uint32_t cache_n = v.cache_n;
   uint32_t fires = 0, nscan = 0;
@@ -1309,11 +1377,19 @@ __device__ __noinline__ void notify_small(const CP<OffT, EstT>& p, const View<Es
   acc.nscan += nscan;
 }
 
+template <typename OffT, typename EstT>
+__device__ __noinline__ void notify_small(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                          const Enq& q, const EstT* s_cache, int c, Acc& acc) {
+  Acc32 a{0, 0, 0, 0, 0, 0, false};
+  notify_small_impl(p, v, q, s_cache, c, a);
+  merge_acc(acc, a);
+}
+
 // THREAD droppers: lane per dropper, TUN droppers per lane per pass, loads
 // issued level by level (estimates, offsets, ids, gathers, counters).
-template <typename OffT, typename EstT>
-__device__ __noinline__ void notify_thread(const CP<OffT, EstT>& p, const View<EstT>& v,
-                                           const Enq& q, const EstT* s_cache, Acc& acc) {
+template <typename OffT, typename EstT, typename A>
+__device__ __forceinline__ void notify_thread_impl(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                           const Enq& q, const EstT* s_cache, A& acc) {
   constexpr int R = DEG_THREAD_MAX;
   const uint32_t cache_n = v.cache_n;
   uint32_t fires = 0, nscan = 0;
@@ -1377,6 +1453,14 @@ __device__ __noinline__ void notify_thread(const CP<OffT, EstT>& p, const View<E
   });
   acc.fires += fires;
   acc.nscan += nscan;
+}
+
+template <typename OffT, typename EstT>
+__device__ __noinline__ void notify_thread(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                           const Enq& q, const EstT* s_cache, Acc& acc) {
+  Acc32 a{0, 0, 0, 0, 0, 0, false};
+  notify_thread_impl(p, v, q, s_cache, a);
+  merge_acc(acc, a);
 }
 
 template <typename OffT, typename EstT>
