@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -75,12 +77,17 @@ kc_status check_device(int device, int* num_sms) {
     return fail(KC_ERR_NO_DEVICE, "no CUDA device available (the B200 path has no CPU fallback)");
   }
   if (device < 0 || device >= count) return fail(KC_ERR_NO_DEVICE, "device index out of range");
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, device));
-  if (prop.major != 10)
+  // single attributes (cudaGetDeviceProperties costs milliseconds per call)
+  int major = 0, sms = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  if (major != 10) {
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
     return fail(KC_ERR_NO_DEVICE, std::string("device is not sm_100 (Blackwell): ") + prop.name);
+  }
   CK(cudaSetDevice(device));
-  if (num_sms) *num_sms = prop.multiProcessorCount;
+  if (num_sms) *num_sms = sms;
   return KC_OK;
 }
 
@@ -372,8 +379,21 @@ kc_status permute_back(kc_graph* g) {
   return KC_OK;
 }
 
+// KC_DEBUG_HOST=1: host wall-clock milestones of the upload (stderr).
+struct HostClock {
+  bool on = std::getenv("KC_DEBUG_HOST") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[kc upload] %-22s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+  }
+};
+
 kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint32_t flags,
                         kc_graph** out) {
+  HostClock hc;
   if (!out) return fail(KC_ERR_INVALID_ARGUMENT, "out is null");
   *out = nullptr;
   if (!csr) return fail(KC_ERR_INVALID_ARGUMENT, "csr view is null");
@@ -382,6 +402,7 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
   int sms = 0;
   kc_status s = check_device(device, &sms);
   if (s != KC_OK) return s;
+  hc.mark("check_device");
   kc_graph* g = new (std::nothrow) kc_graph();
   if (!g) return fail(KC_ERR_OUT_OF_MEMORY, "host allocation failed");
   g->device = device;
@@ -397,6 +418,7 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
     return bail(cuda_fail(e, "cudaStreamCreate"));
   for (auto& ev : g->ev)
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
+  hc.mark("stream+events");
   if (g->n == 0) {
     *out = g;
     return KC_OK;
@@ -424,6 +446,7 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
       return bail(cuda_fail(e, "cudaMemcpy H2D"));
     }
     cudaEventRecord(g->ev[1], g->stream);
+    hc.mark("H2D enqueued");
   } else {
     d_off = const_cast<uint64_t*>(csr->offsets);
     d_adj = const_cast<uint32_t*>(csr->neighbors);
@@ -432,8 +455,10 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
   }
   e = prep_layout(d_off, d_adj, g->n, g->nnz, (flags & KC_UPLOAD_FORCE_OFF64) != 0, g->stream,
                   &g->lay);
+  hc.mark("layout returned");
   cudaEventRecord(g->ev[2], g->stream);
   cudaStreamSynchronize(g->stream);
+  hc.mark("synced");
   if (!on_device) {
     dfree(d_off, g->stream);
     dfree(d_adj, g->stream);
