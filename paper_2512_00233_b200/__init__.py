@@ -30,6 +30,7 @@ from .api import (  # noqa: F401
     RunReport,
     Rule,
     fastk_run,
+    fastk_run_abi,
     gen_config,
     library_path,
     load_library,

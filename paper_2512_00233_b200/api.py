@@ -69,6 +69,7 @@ KC_DEBUG_PHASE_TIMES = 1
 KC_DEBUG_LEGACY_COUNT = 2
 KC_UPLOAD_FORCE_OFF64 = 1
 KC_UPLOAD_FORCE_EST32 = 2
+KC_UPLOAD_UNSORTED_ROWS = 4
 
 _lib = None
 
@@ -450,6 +451,22 @@ def _report(st: dict, trace=None) -> RunReport:
                      tail_pops=int(st["tail_pops"]), trace=trace or [], gpu=st)
 
 
+def fastk_run_abi(g: Graph, options: FastKOptions | None = None,
+                  out: np.ndarray | None = None):
+    """The one-shot C-ABI drop-in, kc_fastk_run: host CSR in (upload, layout,
+    solve, download, free in one call), coreness written to `out` (host).
+    Returns (coreness, stats dict)."""
+    o = (options or FastKOptions())._c()
+    st = _Stats()
+    n = g.node_count()
+    if out is None:
+        out = np.zeros(max(n, 1), dtype=np.uint32)
+    v = g._view()
+    _check(load_library().kc_fastk_run(C.byref(v), C.byref(o), out.ctypes.data, C.byref(st)),
+           "kc_fastk_run")
+    return out[:n], st.as_dict()
+
+
 def fastk_run(g: Graph, options: FastKOptions | None = None,
               instr: Instrumentation | None = None, device: int = 0) -> EngineResult:
     """kcore::fastk_run (fastk.hpp:46-47) on the B200.
@@ -460,7 +477,7 @@ def fastk_run(g: Graph, options: FastKOptions | None = None,
         raise ValueError("fastk: threads must be >= 1")
     if int(options.batch) == 0:
         raise ValueError("fastk: batch must be >= 1")
-    gg = GpuGraph(g, device)
+    gg = GpuGraph(g, device, flags=KC_UPLOAD_UNSORTED_ROWS)  # one solve: no row sort
     try:
         if instr is None or (not instr.trace_convergence and instr.inspector is None):
             core, st = gg.solve(options)

@@ -453,8 +453,8 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
     cudaEventRecord(g->ev[0], g->stream);
     cudaEventRecord(g->ev[1], g->stream);
   }
-  e = prep_layout(d_off, d_adj, g->n, g->nnz, (flags & KC_UPLOAD_FORCE_OFF64) != 0, g->stream,
-                  &g->lay);
+  e = prep_layout(d_off, d_adj, g->n, g->nnz, (flags & KC_UPLOAD_FORCE_OFF64) != 0,
+                  (flags & KC_UPLOAD_UNSORTED_ROWS) == 0, g->stream, &g->lay);
   hc.mark("layout returned");
   cudaEventRecord(g->ev[2], g->stream);
   cudaStreamSynchronize(g->stream);
@@ -517,7 +517,7 @@ kc_status kc_graph_upload_device(const kc_csr_view* csr, int device, kc_graph** 
 kc_status kc_graph_upload_ex(const kc_csr_view* csr, int device, int on_device, uint32_t flags,
                              kc_graph** out) {
   g_last_error.clear();
-  if (flags & ~(KC_UPLOAD_FORCE_OFF64 | KC_UPLOAD_FORCE_EST32))
+  if (flags & ~(KC_UPLOAD_FORCE_OFF64 | KC_UPLOAD_FORCE_EST32 | KC_UPLOAD_UNSORTED_ROWS))
     return fail(KC_ERR_INVALID_ARGUMENT, "unknown upload flags");
   return upload_common(csr, device, on_device != 0, flags, out);
 }
@@ -731,7 +731,8 @@ kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* 
   kc_status s = validate(opt, &o);  // invalid options rejected before any work
   if (s != KC_OK) return s;
   kc_graph* g = nullptr;
-  s = kc_graph_upload(csr, 0, &g);
+  // one solve: the per-row sort of the layout would cost more than it saves
+  s = kc_graph_upload_ex(csr, 0, 0, KC_UPLOAD_UNSORTED_ROWS, &g);
   if (s != KC_OK) return s;
   s = kc_solve(g, &o, coreness, st);
   kc_graph_free(g);

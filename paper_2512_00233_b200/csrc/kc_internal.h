@@ -140,6 +140,6 @@ struct PrepOut {
   bool off64;
 };
 cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, uint64_t nnz,
-                        bool force_off64, cudaStream_t s, PrepOut* out);
+                        bool force_off64, bool sort_rows, cudaStream_t s, PrepOut* out);
 
 }  // namespace kcb

@@ -63,8 +63,9 @@ EngineResult fastk_run(const Graph& g, const FastKOptions& opt, const Instrument
   std::vector<uint32_t> core(n);
   kc_stats st{};
   kc_graph* h = nullptr;
-  kc_status s = kc_graph_upload(&view, 0, &h);
-  if (s != KC_OK) raise(s, "kc_graph_upload");
+  // one solve per call: unsorted rows (the row sort costs more than it saves)
+  kc_status s = kc_graph_upload_ex(&view, 0, 0, KC_UPLOAD_UNSORTED_ROWS, &h);
+  if (s != KC_OK) raise(s, "kc_graph_upload_ex");
   const bool observed = instr && (instr->trace_convergence || instr->inspector);
   if (observed) {
     HookCtx ctx{&out.report, instr};

@@ -18,6 +18,7 @@ desc, (p0, p1, p2), seed = CONFIGS[a.config]
 if a.scale: p0 = a.scale
 d = K.gen_config(a.config, p0, p1, p2, seed=seed)
 g = K.GpuGraph(d)
+print("upload/prep ms", g.timings(), flush=True)
 for i in range(a.reps):
     o = K.FastKOptions(rule=K.Rule(a.rule), smem_cache=a.cache)
     if a.legacy:

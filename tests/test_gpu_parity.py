@@ -239,10 +239,10 @@ def test_long_path_many_rounds(gpu):
 
 
 # ---------------------------------------------------------------- layouts
-@pytest.mark.parametrize("flags", [0, 1, 2, 3])
+@pytest.mark.parametrize("flags", list(range(8)))
 def test_layout_variants(gpu, oracle, flags):
     """All four kernel instantiations (uint32/uint64 offsets x uint16/uint32
-    estimates) give the same coreness."""
+    estimates), with sorted and unsorted rows, give the same coreness."""
     g = oracle.build_csr(1 << 14, oracle.gen_rmat(14, 16, 7))
     truth = oracle.peel(g)
     gg = gpu.GpuGraph(to_graph(gpu, g), flags=flags)
@@ -318,6 +318,20 @@ def test_full_size_configs_vs_golden(gpu, cfg):
         assert np.array_equal(core, core3)
         want = d["reference_fastk_default"]
         assert {k: st3[k] for k in want} == want
+
+
+def test_one_shot_abi_matches_handle_path(gpu, oracle):
+    """kc_fastk_run (unsorted rows) == upload handle + kc_solve (sorted rows),
+    counters included (the Jacobi trajectory does not depend on row order)."""
+    g = oracle.build_csr(1 << 15, oracle.gen_rmat(15, 16, 11))
+    G = to_graph(gpu, g)
+    for rule in RULES:
+        o = gpu.FastKOptions(rule=gpu.Rule[rule])
+        core1, st1 = gpu.fastk_run_abi(G, o)
+        core2, st2 = gpu.GpuGraph(G).solve(o)
+        assert np.array_equal(core1, core2) and np.array_equal(core1, oracle.peel(g))
+        keys = ("iterations", "messages_sent", "messages_drained", "tail_pops", "e_scan")
+        assert {k: st1[k] for k in keys} == {k: st2[k] for k in keys}
 
 
 def test_invalid_arguments_on_device(gpu):
