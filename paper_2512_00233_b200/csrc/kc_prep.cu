@@ -101,6 +101,36 @@ __global__ void relabel_rows_kernel(const uint64_t* __restrict__ old_off,
   }
 }
 
+// Rows of degree <= 64 (new ids [first, n_nz), the tail of the degree-sorted
+// order): 8-lane tile per row, up to 8 entries per lane — no per-row search.
+template <typename OffT>
+__global__ void relabel_small_rows_kernel(const uint64_t* __restrict__ old_off,
+                                          const uint32_t* __restrict__ old_adj,
+                                          const uint32_t* __restrict__ perm,
+                                          const uint32_t* __restrict__ inv, uint32_t first,
+                                          uint32_t n_nz, const OffT* __restrict__ new_off,
+                                          uint32_t* __restrict__ new_adj) {
+  const uint32_t k = threadIdx.x & 7;
+  const uint64_t t0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 3;
+  const uint64_t nt = (gridDim.x * (uint64_t)blockDim.x) >> 3;
+  for (uint64_t i = first + t0; i < n_nz; i += nt) {
+    const uint64_t b = (uint64_t)new_off[i];
+    const uint32_t deg = (uint32_t)((uint64_t)new_off[i + 1] - b);
+    const uint32_t* src = old_adj + old_off[perm[i]];
+    uint32_t v[DEG_SUB_MAX / 8];
+#pragma unroll
+    for (int j = 0; j < (int)(DEG_SUB_MAX / 8); ++j) {
+      const uint32_t e = k + 8u * j;
+      v[j] = e < deg ? src[e] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < (int)(DEG_SUB_MAX / 8); ++j) {
+      const uint32_t e = k + 8u * j;
+      if (e < deg) new_adj[b + e] = inv[v[j]];
+    }
+  }
+}
+
 template <typename OffT>
 __global__ void chunk_count_kernel(const OffT* __restrict__ new_off, uint32_t n_nz,
                                    uint64_t* __restrict__ chunks) {
@@ -199,34 +229,48 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
     }
     PREP_CK(dalloc(&new_adj, nnz + ADJ_PAD, s));
     PREP_CK(cudaMemsetAsync(new_adj + nnz, 0, ADJ_PAD * sizeof(uint32_t), s));
-    PREP_CK(dalloc(&chunks, (size_t)n_nz + 1, s));
-    if (n_nz) {
+    // rows of degree > 64 (ids [0, n_big)) are cut into 1024-entry chunks
+    // for warps; the rest take the 8-lane-per-row kernel
+    const uint32_t n_big = out->cls_begin[C_SUB];
+    if (n_nz > n_big) {
       if (off64)
-        chunk_count_kernel<uint64_t><<<G, B, 0, s>>>((const uint64_t*)new_off, n_nz, chunks);
+        relabel_small_rows_kernel<uint64_t><<<G, B, 0, s>>>(off, adj, perm, inv, n_big, n_nz,
+                                                            (const uint64_t*)new_off, new_adj);
       else
-        chunk_count_kernel<uint32_t><<<G, B, 0, s>>>((const uint32_t*)new_off, n_nz, chunks);
+        relabel_small_rows_kernel<uint32_t><<<G, B, 0, s>>>(off, adj, perm, inv, n_big, n_nz,
+                                                            (const uint32_t*)new_off, new_adj);
+      PREP_CK(cudaGetLastError());
+    }
+    PREP_CK(dalloc(&chunks, (size_t)n_big + 1, s));
+    if (n_big) {
+      if (off64)
+        chunk_count_kernel<uint64_t><<<G, B, 0, s>>>((const uint64_t*)new_off, n_big, chunks);
+      else
+        chunk_count_kernel<uint32_t><<<G, B, 0, s>>>((const uint32_t*)new_off, n_big, chunks);
       PREP_CK(cudaGetLastError());
       size_t nb = 0;
-      PREP_CK(cub::DeviceScan::ExclusiveSum(nullptr, nb, chunks, chunks, n_nz + 1, s));
+      PREP_CK(cub::DeviceScan::ExclusiveSum(nullptr, nb, chunks, chunks, n_big + 1, s));
       if (nb > tmp_bytes) {
         dfree(tmp, s);
         tmp = nullptr;
         tmp_bytes = nb;
         PREP_CK(dmalloc(&tmp, tmp_bytes, s));
       }
-      // chunks[n_nz] must be 0 before the exclusive scan so the total lands there
-      PREP_CK(cudaMemsetAsync(chunks + n_nz, 0, sizeof(uint64_t), s));
-      PREP_CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, chunks, chunks, n_nz + 1, s));
+      // chunks[n_big] must be 0 before the exclusive scan so the total lands there
+      PREP_CK(cudaMemsetAsync(chunks + n_big, 0, sizeof(uint64_t), s));
+      PREP_CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, chunks, chunks, n_big + 1, s));
       uint64_t total = 0;
-      PREP_CK(cudaMemcpyAsync(&total, chunks + n_nz, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      PREP_CK(cudaMemcpyAsync(&total, chunks + n_big, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
       PREP_CK(cudaStreamSynchronize(s));
       if (off64)
-        relabel_rows_kernel<uint64_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_nz,
+        relabel_rows_kernel<uint64_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_big,
                                                       (const uint64_t*)new_off, new_adj, total);
       else
-        relabel_rows_kernel<uint32_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_nz,
+        relabel_rows_kernel<uint32_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_big,
                                                       (const uint32_t*)new_off, new_adj, total);
       PREP_CK(cudaGetLastError());
+    }
+    {
       // sort each row ascending (segmented sort over the new offsets)
       if (KC_PREP_SORT && sort_rows && nnz > 0 && nnz < (1ull << 31)) {
         PREP_CK(dalloc(&sort_tmp, nnz + ADJ_PAD, s));
