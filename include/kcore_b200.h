@@ -145,6 +145,23 @@ kc_status kc_solve_device(kc_graph* g, const kc_options* opt, uint32_t* coreness
 kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn fn,
                             void* user, uint32_t* coreness, kc_stats* stats);
 
+/* Convergence trace computed on the device (record_iteration,
+ * /root/reference/proj/src/report.cpp:7-18; IterationStat, report.hpp:14-17):
+ * one row per iteration boundary (iteration 0 = degrees, then every executed
+ * round, plus the tail boundary under the hybrid tail), mean_error = mean of
+ * (estimate - truth), active_fraction = active / n.  Per boundary only a
+ * 16-byte reduction result crosses PCIe, never the estimates.  The gap is
+ * summed exactly, so the doubles equal the reference's.  `truth` is a HOST
+ * array of n coreness values (caller ids); rows beyond trace_cap are counted
+ * in *trace_rows but not written. */
+typedef struct kc_iteration_stat {
+  double mean_error;
+  double active_fraction;
+} kc_iteration_stat;
+kc_status kc_solve_traced(kc_graph* g, const kc_options* opt, const uint32_t* truth,
+                          kc_iteration_stat* trace, uint64_t trace_cap, uint64_t* trace_rows,
+                          uint32_t* coreness, kc_stats* stats);
+
 /* One-shot drop-in: upload (KC_UPLOAD_UNSORTED_ROWS) + solve + download + free
  * (fastk_run semantics). */
 kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* coreness,

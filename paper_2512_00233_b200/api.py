@@ -63,7 +63,7 @@ ABI_SYMBOLS = (
     "kc_graph_nnz", "kc_graph_timings", "kc_solve", "kc_solve_device",
     "kc_solve_observed", "kc_fastk_run", "kc_graph_stream", "kc_gen_config",
     "kc_csr_dev_free", "kc_csr_dev_download", "kc_debug_phase_times", "kc_graph_upload_ex",
-    "kc_debug_round_stats",
+    "kc_debug_round_stats", "kc_solve_traced",
 )
 KC_DEBUG_PHASE_TIMES = 1
 KC_DEBUG_LEGACY_COUNT = 2
@@ -116,6 +116,10 @@ def load_library():
     L.kc_solve_observed.restype = C.c_int
     L.kc_solve_observed.argtypes = [C.c_void_p, C.POINTER(_Options), _INSPECTOR, C.c_void_p,
                                     C.c_void_p, C.POINTER(_Stats)]
+    L.kc_solve_traced.restype = C.c_int
+    L.kc_solve_traced.argtypes = [C.c_void_p, C.POINTER(_Options), C.c_void_p, C.c_void_p,
+                                  C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p,
+                                  C.POINTER(_Stats)]
     L.kc_fastk_run.restype = C.c_int
     L.kc_fastk_run.argtypes = [C.POINTER(_CSRView), C.POINTER(_Options), C.c_void_p,
                                C.POINTER(_Stats)]
@@ -416,6 +420,31 @@ class GpuGraph:
         _check(status, "kc_solve_observed")
         return out[: self.n], st.as_dict()
 
+    def solve_traced(self, options: FastKOptions | None, truth):
+        """Convergence trace on the device (kc_solve_traced; record_iteration,
+        report.cpp:7-18): returns (coreness, stats, [IterationStat])."""
+        o = (options or FastKOptions())._c()
+        st = _Stats()
+        out = np.zeros(max(self.n, 1), dtype=np.uint32)
+        tr = np.ascontiguousarray(truth, dtype=np.uint32)
+        if tr.size != self.n:
+            raise ValueError("truth must hold one coreness per vertex")
+        cap = 4096
+        rows = np.zeros((cap, 2), dtype=np.float64)
+        nrows = C.c_uint64()
+        _check(load_library().kc_solve_traced(self._h, C.byref(o), tr.ctypes.data, rows.ctypes.data,
+                                              cap, C.byref(nrows), out.ctypes.data, C.byref(st)),
+               "kc_solve_traced")
+        if nrows.value > cap:  # long runs: once more with room for every row
+            cap = int(nrows.value)
+            rows = np.zeros((cap, 2), dtype=np.float64)
+            _check(load_library().kc_solve_traced(self._h, C.byref(o), tr.ctypes.data,
+                                                  rows.ctypes.data, cap, C.byref(nrows),
+                                                  out.ctypes.data, C.byref(st)),
+                   "kc_solve_traced")
+        trace = [IterationStat(float(a), float(b)) for a, b in rows[: nrows.value]]
+        return out[: self.n], st.as_dict(), trace
+
     def phase_times(self) -> np.ndarray:
         """[256 rounds, grid, 8] %globaltimer stamps (debug; KC_DEBUG_PHASE_TIMES)."""
         grid = C.c_uint32()
@@ -490,6 +519,10 @@ def fastk_run(g: Graph, options: FastKOptions | None = None,
             if instr.truth is None:
                 raise ValueError("trace_convergence requires truth")
             truth = np.asarray(instr.truth.coreness, dtype=np.float64)
+            if instr.inspector is None:  # trace only: reductions on the device
+                core, st, trace = gg.solve_traced(options, instr.truth.coreness)
+                return EngineResult(CorenessResult(core, int(st["k_max"]), float(st["k_avg"])),
+                                    _report(st, trace))
 
         def hook(it, est, active):
             if truth is not None:  # record_iteration, report.cpp:7-18

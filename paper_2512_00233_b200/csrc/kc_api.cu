@@ -619,8 +619,70 @@ kc_status kc_solve_device(kc_graph* g, const kc_options* opt, uint32_t* coreness
   return solve_impl(g, opt, coreness_dev, true, st);
 }
 
-kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn fn, void* user,
-                            uint32_t* coreness, kc_stats* st) {
+}  // extern "C"
+
+namespace {
+
+// What the one-round-per-launch loop hands out at each iteration boundary
+// (instrument_boundary, report.cpp:20-29): the estimates to an inspector
+// (one D2H of est per boundary), and/or a record_iteration row
+// (report.cpp:7-18) computed on the device — a sum of the estimates, so a
+// trace costs one 16-byte copy per boundary.  The gap sum is an exact
+// integer, so mean_error is bit-identical to the reference's double sum.
+struct Boundaries {
+  kc_inspector_fn fn = nullptr;
+  void* user = nullptr;
+  bool trace = false;
+  uint64_t truth_sum = 0;
+  kc_iteration_stat* rows = nullptr;
+  uint64_t cap = 0;
+  uint64_t count = 0;
+};
+
+kc_status boundary(kc_graph* g, Boundaries& b, uint64_t it, uint64_t active,
+                   std::vector<uint32_t>& snap, bool degrees) {
+  if (b.fn) {
+    if (degrees) {  // iteration 0: the reference reports est = degree (fastk.cpp:67-68, 93)
+      if (g->lay.off64)
+        degree_back_kernel<uint64_t><<<g->num_sms * 4, 256, 0, g->stream>>>(
+            (const uint64_t*)g->lay.off, g->lay.perm, g->n, g->lay.n_nz, g->d_out);
+      else
+        degree_back_kernel<uint32_t><<<g->num_sms * 4, 256, 0, g->stream>>>(
+            (const uint32_t*)g->lay.off, g->lay.perm, g->n, g->lay.n_nz, g->d_out);
+      CK(cudaGetLastError());
+    } else {
+      kc_status s = permute_back(g);
+      if (s != KC_OK) return s;
+    }
+    CK(cudaMemcpyAsync(snap.data(), g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                       g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    if (b.fn(b.user, it, snap.data(), g->n, active)) return fail(KC_ERR_CALLBACK, "inspector");
+  }
+  if (b.trace) {
+    uint64_t sum = g->nnz;  // iteration 0: sum of degrees
+    if (!degrees) {
+      unsigned long long k[2] = {0, 0};
+      CK(cudaMemsetAsync(g->d_k, 0, sizeof(k), g->stream));
+      kstats_kernel<<<g->num_sms * 2, 256, 0, g->stream>>>(g->sb.est[g->state_buf], g->est16,
+                                                          g->lay.n_nz, g->d_k);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(k, g->d_k, sizeof(k), cudaMemcpyDeviceToHost, g->stream));
+      CK(cudaStreamSynchronize(g->stream));
+      sum = k[1];
+    }
+    if (b.count < b.cap) {
+      const double n = (double)g->n;
+      b.rows[b.count].mean_error = g->n ? (double)((int64_t)sum - (int64_t)b.truth_sum) / n : 0.0;
+      b.rows[b.count].active_fraction = g->n ? (double)active / n : 0.0;
+    }
+    ++b.count;
+  }
+  return KC_OK;
+}
+
+kc_status observed_impl(kc_graph* g, const kc_options* opt, Boundaries& b, uint32_t* coreness,
+                        kc_stats* st) {
   g_last_error.clear();
   if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
   kc_options o;
@@ -629,11 +691,19 @@ kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn 
   if (g->n && !coreness) return fail(KC_ERR_INVALID_ARGUMENT, "coreness is null");
   if (st) std::memset(st, 0, sizeof(*st));
   CK(cudaSetDevice(g->device));
-  std::vector<uint32_t> snap(g->n);
+  std::vector<uint32_t> snap(b.fn ? g->n : 0);
   if (g->n == 0 || g->lay.n_nz == 0) {
     // iteration 0 (degrees = 0) and the single quiescent round
-    if (fn && fn(user, 0, snap.data(), g->n, g->n)) return fail(KC_ERR_CALLBACK, "inspector");
-    if (fn && fn(user, 1, snap.data(), g->n, 0)) return fail(KC_ERR_CALLBACK, "inspector");
+    if (b.fn && b.fn(b.user, 0, snap.data(), g->n, g->n)) return fail(KC_ERR_CALLBACK, "inspector");
+    if (b.fn && b.fn(b.user, 1, snap.data(), g->n, 0)) return fail(KC_ERR_CALLBACK, "inspector");
+    for (uint64_t it = 0; b.trace && it < 2; ++it) {
+      if (b.count < b.cap) {
+        const double n = g->n ? (double)g->n : 1.0;
+        b.rows[b.count].mean_error = -(double)b.truth_sum / n;
+        b.rows[b.count].active_fraction = it == 0 && g->n ? 1.0 : 0.0;
+      }
+      ++b.count;
+    }
     if (g->n) std::memset(coreness, 0, g->n * sizeof(uint32_t));
     if (st) {
       st->iterations = 1;
@@ -645,17 +715,8 @@ kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn 
   if (s != KC_OK) return s;
   s = init_state(g, o);
   if (s != KC_OK) return s;
-  // iteration 0: the reference reports est = degree (fastk.cpp:67-68, 93)
-  if (g->lay.off64)
-    degree_back_kernel<uint64_t><<<g->num_sms * 4, 256, 0, g->stream>>>(
-        (const uint64_t*)g->lay.off, g->lay.perm, g->n, g->lay.n_nz, g->d_out);
-  else
-    degree_back_kernel<uint32_t><<<g->num_sms * 4, 256, 0, g->stream>>>(
-        (const uint32_t*)g->lay.off, g->lay.perm, g->n, g->lay.n_nz, g->d_out);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(snap.data(), g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
-  CK(cudaStreamSynchronize(g->stream));
-  if (fn && fn(user, 0, snap.data(), g->n, g->n)) return fail(KC_ERR_CALLBACK, "inspector");
+  s = boundary(g, b, 0, g->n, snap, true);
+  if (s != KC_OK) return s;
   bool conv = false;
   for (uint32_t r = 0; r < o.max_rounds && !conv; ++r) {
     s = run_rounds(g, o, r, r + 1, false);
@@ -675,26 +736,18 @@ kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn 
                                                                 g->lay.n_nz, g->d_count);
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(&active, g->d_count, sizeof(active), cudaMemcpyDeviceToHost, g->stream));
+      CK(cudaStreamSynchronize(g->stream));
     }
-    s = permute_back(g);
+    s = boundary(g, b, (uint64_t)r + 1, active, snap, false);
     if (s != KC_OK) return s;
-    CK(cudaMemcpyAsync(snap.data(), g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
-    CK(cudaStreamSynchronize(g->stream));
-    if (fn && fn(user, (uint64_t)r + 1, snap.data(), g->n, active))
-      return fail(KC_ERR_CALLBACK, "inspector");
     if (!conv && uses_tail(o) && active < o.batch) {
       // hybrid switch after round r (fastk.cpp:113-115): the sequential tail
       // from round r+1's active flags, then one more boundary with nothing
       // active (fastk.cpp:180-183)
       CK(launch_tail(g->sb, g->lay.perm, g->est16, g->lay.off64, o.extended_notify != 0,
                      (int)((r + 1) & 1), g->num_sms, g->stream));
-      s = permute_back(g);
+      s = boundary(g, b, (uint64_t)r + 2, 0, snap, false);
       if (s != KC_OK) return s;
-      CK(cudaMemcpyAsync(snap.data(), g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                         g->stream));
-      CK(cudaStreamSynchronize(g->stream));
-      if (fn && fn(user, (uint64_t)r + 2, snap.data(), g->n, 0))
-        return fail(KC_ERR_CALLBACK, "inspector");
       conv = true;
     }
   }
@@ -703,9 +756,43 @@ kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn 
   if (s != KC_OK) return s;
   s = kstats(g, st);
   if (s != KC_OK) return s;
-  std::memcpy(coreness, snap.data(), g->n * sizeof(uint32_t));
+  s = permute_back(g);
+  if (s != KC_OK) return s;
+  CK(cudaMemcpyAsync(coreness, g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                     g->stream));
+  CK(cudaStreamSynchronize(g->stream));
   return KC_OK;
 }
+
+}  // namespace
+
+extern "C" {
+
+kc_status kc_solve_observed(kc_graph* g, const kc_options* opt, kc_inspector_fn fn, void* user,
+                            uint32_t* coreness, kc_stats* st) {
+  Boundaries b;
+  b.fn = fn;
+  b.user = user;
+  return observed_impl(g, opt, b, coreness, st);
+}
+
+kc_status kc_solve_traced(kc_graph* g, const kc_options* opt, const uint32_t* truth,
+                          kc_iteration_stat* trace, uint64_t trace_cap, uint64_t* trace_rows,
+                          uint32_t* coreness, kc_stats* st) {
+  if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
+  if (g->n && !truth) return fail(KC_ERR_INVALID_ARGUMENT, "truth is null");
+  if (trace_cap && !trace) return fail(KC_ERR_INVALID_ARGUMENT, "trace is null");
+  Boundaries b;
+  b.trace = true;
+  for (uint32_t u = 0; u < g->n; ++u) b.truth_sum += truth[u];
+  b.rows = trace;
+  b.cap = trace_cap;
+  kc_status s = observed_impl(g, opt, b, coreness, st);
+  if (trace_rows) *trace_rows = b.count;
+  return s;
+}
+
+
 
 kc_status kc_debug_phase_times(kc_graph* g, unsigned long long* out, uint64_t cap,
                                uint32_t* grid) {

@@ -67,7 +67,24 @@ EngineResult fastk_run(const Graph& g, const FastKOptions& opt, const Instrument
   kc_status s = kc_graph_upload_ex(&view, 0, 0, KC_UPLOAD_UNSORTED_ROWS, &h);
   if (s != KC_OK) raise(s, "kc_graph_upload_ex");
   const bool observed = instr && (instr->trace_convergence || instr->inspector);
-  if (observed) {
+  if (observed && !instr->inspector) {
+    // trace only: record_iteration's rows reduced on the device
+    if (!instr->truth) {
+      kc_graph_free(h);
+      throw std::invalid_argument("fastk: trace_convergence requires truth");
+    }
+    std::vector<kc_iteration_stat> rows(4096);
+    uint64_t nrows = 0;
+    s = kc_solve_traced(h, &o, instr->truth->coreness.data(), rows.data(), rows.size(), &nrows,
+                        core.data(), &st);
+    if (s == KC_OK && nrows > rows.size()) {
+      rows.resize(nrows);
+      s = kc_solve_traced(h, &o, instr->truth->coreness.data(), rows.data(), rows.size(), &nrows,
+                          core.data(), &st);
+    }
+    for (uint64_t i = 0; s == KC_OK && i < nrows; ++i)
+      out.report.trace.push_back(IterationStat{rows[i].mean_error, rows[i].active_fraction});
+  } else if (observed) {
     HookCtx ctx{&out.report, instr};
     s = kc_solve_observed(h, &o, &on_boundary, &ctx, core.data(), &st);
   } else {
