@@ -70,6 +70,7 @@ typedef struct kc_options {
 
 #define KC_DEBUG_PHASE_TIMES 1u /* record per-CTA per-round phase timestamps */
 #define KC_DEBUG_LEGACY_COUNT 2u /* counting rule on the flag-frontier solver (A/B) */
+#define KC_DEBUG_VERIFY_PERTURB 4u /* kc_verify self-test: candidate[u] += 1 for u % 997 == 0 */
 
 /* RunReport (report.hpp:17-23) + work counters and timings. */
 typedef struct kc_stats {
@@ -161,6 +162,25 @@ typedef struct kc_iteration_stat {
 kc_status kc_solve_traced(kc_graph* g, const kc_options* opt, const uint32_t* truth,
                           kc_iteration_stat* trace, uint64_t trace_cap, uint64_t* trace_rows,
                           uint32_t* coreness, kc_stats* stats);
+
+/* ---- independent checker on the device ------------ */
+/* kcore::peel_coreness (/root/reference/proj/src/oracle.cpp:21-66) as a
+ * separate device algorithm (level-synchronous parallel peel, kc_peel.cu;
+ * shares nothing with the FastK kernels but the layout).  coreness[n] to
+ * HOST memory (caller ids); stats: iterations = peel levels (k_max + 1),
+ * k_max, k_avg, t_solve_ms = device time of the peel. */
+kc_status kc_peel(kc_graph* g, uint32_t* coreness, kc_stats* stats);
+/* kcore::verify (oracle.cpp:68-75) on the device: FastK under `opt` and the
+ * device peel on the same handle, compared on the device.  *count = number of
+ * mismatching vertices; the first min(cap, count) in ascending node id go to
+ * out[] (Mismatch, oracle.hpp:23-27).  Only the mismatches cross PCIe. */
+typedef struct kc_mismatch {
+  uint32_t node;
+  uint32_t candidate;
+  uint32_t truth;
+} kc_mismatch;
+kc_status kc_verify(kc_graph* g, const kc_options* opt, kc_mismatch* out, uint64_t cap,
+                    uint64_t* count);
 
 /* One-shot drop-in: upload (KC_UPLOAD_UNSORTED_ROWS) + solve + download + free
  * (fastk_run semantics). */

@@ -63,10 +63,11 @@ ABI_SYMBOLS = (
     "kc_graph_nnz", "kc_graph_timings", "kc_solve", "kc_solve_device",
     "kc_solve_observed", "kc_fastk_run", "kc_graph_stream", "kc_gen_config",
     "kc_csr_dev_free", "kc_csr_dev_download", "kc_debug_phase_times", "kc_graph_upload_ex",
-    "kc_debug_round_stats", "kc_solve_traced",
+    "kc_debug_round_stats", "kc_solve_traced", "kc_peel", "kc_verify",
 )
 KC_DEBUG_PHASE_TIMES = 1
 KC_DEBUG_LEGACY_COUNT = 2
+KC_DEBUG_VERIFY_PERTURB = 4
 KC_UPLOAD_FORCE_OFF64 = 1
 KC_UPLOAD_FORCE_EST32 = 2
 KC_UPLOAD_UNSORTED_ROWS = 4
@@ -120,6 +121,11 @@ def load_library():
     L.kc_solve_traced.argtypes = [C.c_void_p, C.POINTER(_Options), C.c_void_p, C.c_void_p,
                                   C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p,
                                   C.POINTER(_Stats)]
+    L.kc_peel.restype = C.c_int
+    L.kc_peel.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Stats)]
+    L.kc_verify.restype = C.c_int
+    L.kc_verify.argtypes = [C.c_void_p, C.POINTER(_Options), C.c_void_p, C.c_uint64,
+                            C.POINTER(C.c_uint64)]
     L.kc_fastk_run.restype = C.c_int
     L.kc_fastk_run.argtypes = [C.POINTER(_CSRView), C.POINTER(_Options), C.c_void_p,
                                C.POINTER(_Stats)]
@@ -444,6 +450,26 @@ class GpuGraph:
                    "kc_solve_traced")
         trace = [IterationStat(float(a), float(b)) for a, b in rows[: nrows.value]]
         return out[: self.n], st.as_dict(), trace
+
+    def peel(self):
+        """kcore::peel_coreness (oracle.cpp:21-66) as an independent device
+        algorithm (kc_peel): returns (coreness, stats; iterations = levels)."""
+        st = _Stats()
+        out = np.zeros(max(self.n, 1), dtype=np.uint32)
+        _check(load_library().kc_peel(self._h, out.ctypes.data, C.byref(st)), "kc_peel")
+        return out[: self.n], st.as_dict()
+
+    def verify(self, options: FastKOptions | None = None, cap: int = 1024):
+        """kcore::verify (oracle.cpp:68-75) on the device: FastK vs the device
+        peel.  Returns (mismatch count, [(node, candidate, truth)] ascending,
+        at most `cap`)."""
+        o = (options or FastKOptions())._c()
+        out = np.zeros((max(cap, 1), 3), dtype=np.uint32)
+        cnt = C.c_uint64()
+        _check(load_library().kc_verify(self._h, C.byref(o), out.ctypes.data, cap, C.byref(cnt)),
+               "kc_verify")
+        m = min(cap, cnt.value)
+        return int(cnt.value), [tuple(int(x) for x in r) for r in out[:m]]
 
     def phase_times(self) -> np.ndarray:
         """[256 rounds, grid, 8] %globaltimer stamps (debug; KC_DEBUG_PHASE_TIMES)."""

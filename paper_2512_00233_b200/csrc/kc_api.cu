@@ -160,9 +160,29 @@ struct kc_graph {
   unsigned long long* d_count = nullptr; // observed mode: active-flag count
   uint32_t state_buf = 0;                // est buffer holding the current state
   unsigned long long* d_k = nullptr;
+  // independent peel / verify (allocated at first use)
+  bool peel_ready = false;
+  PeelBuffers pb{};
+  uint32_t* d_cand = nullptr;            // verify: FastK coreness (caller ids)
 };
 
 namespace {
+
+void free_peel(kc_graph* g) {
+  if (!g->peel_ready) return;
+  dfree(g->pb.deg, g->stream);
+  dfree(g->pb.core, g->stream);
+  for (int i = 0; i < 2; ++i) {
+    dfree(g->pb.rem[i], g->stream);
+    dfree(g->pb.fr[i], g->stream);
+    dfree(g->pb.frb[i], g->stream);
+  }
+  dfree(g->pb.ctl, g->stream);
+  dfree(g->d_cand, g->stream);
+  g->d_cand = nullptr;
+  std::memset(&g->pb, 0, sizeof(g->pb));
+  g->peel_ready = false;
+}
 
 void free_solver(kc_graph* g) {
   if (!g->solver_ready) return;
@@ -190,6 +210,8 @@ void free_solver(kc_graph* g) {
   dfree(g->d_count, g->stream);
   g->d_prof = nullptr;
   g->d_count = nullptr;
+  g->d_out = nullptr;
+  g->d_k = nullptr;
   std::memset(&g->sb, 0, sizeof(g->sb));
   g->solver_ready = false;
 }
@@ -233,8 +255,8 @@ kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
   CK(dmalloc((void**)&b.stats, (size_t)STAT_SLOTS * sizeof(RoundStat), g->stream));
   CK(dmalloc((void**)&b.status, 4 * sizeof(uint32_t), g->stream));
   CK(dmalloc((void**)&b.tailc, TAIL_SLOTS * sizeof(unsigned long long), g->stream));
-  CK(dmalloc((void**)&g->d_out, (g->n ? g->n : 1) * sizeof(uint32_t), g->stream));
-  CK(dmalloc((void**)&g->d_k, 2 * sizeof(unsigned long long), g->stream));
+  if (!g->d_out) CK(dmalloc((void**)&g->d_out, (g->n ? g->n : 1) * sizeof(uint32_t), g->stream));
+  if (!g->d_k) CK(dmalloc((void**)&g->d_k, 2 * sizeof(unsigned long long), g->stream));
   CK(dmalloc((void**)&g->d_count, sizeof(unsigned long long), g->stream));
   g->max_rounds = max_rounds;
   return KC_OK;
@@ -526,6 +548,9 @@ void kc_graph_free(kc_graph* g) {
   if (!g) return;
   cudaSetDevice(g->device);
   free_solver(g);
+  free_peel(g);
+  dfree(g->d_out, g->stream);  // when only the peel ran
+  dfree(g->d_k, g->stream);
   dfree(g->lay.off, g->stream);
   dfree(g->lay.adj, g->stream);
   dfree(g->lay.perm, g->stream);
@@ -809,6 +834,133 @@ kc_status kc_debug_round_stats(kc_graph* g, unsigned long long* out, uint32_t ro
   if (!g->sb.stats) return fail(KC_ERR_INVALID_ARGUMENT, "no solve has run");
   const uint32_t k = rounds < STAT_SLOTS ? rounds : STAT_SLOTS;
   CK(cudaMemcpy(out, g->sb.stats, (size_t)k * sizeof(RoundStat), cudaMemcpyDeviceToHost));
+  return KC_OK;
+}
+
+static kc_status ensure_peel(kc_graph* g) {
+  if (g->peel_ready) return KC_OK;
+  const size_t m = (size_t)g->lay.n_nz + 1;
+  PeelBuffers& b = g->pb;
+  std::memset(&b, 0, sizeof(b));
+  b.off = g->lay.off;
+  b.adj = g->lay.adj;
+  b.n_nz = g->lay.n_nz;
+  g->peel_ready = true;  // partial allocations get freed
+  CK(dmalloc_n(&b.deg, m, g->stream));
+  CK(dmalloc_n(&b.core, m, g->stream));
+  for (int i = 0; i < 2; ++i) {
+    CK(dmalloc_n(&b.rem[i], m, g->stream));
+    CK(dmalloc_n(&b.fr[i], m, g->stream));
+    CK(dmalloc_n(&b.frb[i], m, g->stream));
+  }
+  CK(dmalloc(&b.ctl, peel_ctl_bytes(), g->stream));
+  CK(dmalloc_n(&g->d_cand, (size_t)g->n + 1, g->stream));
+  if (!g->d_out) CK(dmalloc_n(&g->d_out, (size_t)g->n + 1, g->stream));
+  if (!g->d_k) CK(dmalloc_n(&g->d_k, 2, g->stream));
+  return KC_OK;
+}
+
+// Peel on the device into g->d_out (caller ids); levels and time in st.
+static kc_status peel_device(kc_graph* g, kc_stats* st) {
+  kc_status s = ensure_peel(g);
+  if (s != KC_OK) return s;
+  CK(cudaEventRecord(g->ev[0], g->stream));
+  CK(launch_peel(g->pb, g->lay.off64, g->num_sms, g->stream));
+  CK(cudaEventRecord(g->ev[1], g->stream));
+  CK(launch_peel_out(g->pb, g->lay.perm, g->n, g->d_out, g->num_sms, g->stream));
+  if (st) {
+    uint32_t levels = 0;
+    unsigned long long k[2] = {0, 0};
+    CK(cudaMemcpyAsync(&levels, (const char*)g->pb.ctl + peel_ctl_bytes() - sizeof(uint32_t),
+                       sizeof(levels), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaMemsetAsync(g->d_k, 0, sizeof(k), g->stream));
+    kstats_kernel<<<g->num_sms * 2, 256, 0, g->stream>>>(g->d_out, false, g->n, g->d_k);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(k, g->d_k, sizeof(k), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    st->iterations = g->lay.n_nz ? levels : 1;
+    st->k_max = (uint32_t)k[0];
+    st->k_avg = g->n ? (double)k[1] / (double)g->n : 0.0;
+    st->h_graph = g->lay.h_graph;
+    cudaEventElapsedTime(&st->t_solve_ms, g->ev[0], g->ev[1]);
+  }
+  return KC_OK;
+}
+
+__global__ void perturb_kernel(uint32_t* c, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (i % 997u == 0) c[i] += 1;
+}
+
+__global__ void mismatch_gather_kernel(const uint32_t* ids, uint32_t m, const uint32_t* cand,
+                                       const uint32_t* truth, kc_mismatch* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const uint32_t u = ids[i];
+    out[i].node = u;
+    out[i].candidate = cand[u];
+    out[i].truth = truth[u];
+  }
+}
+
+kc_status kc_peel(kc_graph* g, uint32_t* coreness, kc_stats* st) {
+  g_last_error.clear();
+  if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
+  if (g->n && !coreness) return fail(KC_ERR_INVALID_ARGUMENT, "coreness is null");
+  if (st) std::memset(st, 0, sizeof(*st));
+  CK(cudaSetDevice(g->device));
+  if (g->n == 0) {
+    if (st) st->iterations = 1;
+    return KC_OK;
+  }
+  kc_status s = peel_device(g, st);
+  if (s != KC_OK) return s;
+  CK(cudaMemcpyAsync(coreness, g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                     g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  return KC_OK;
+}
+
+kc_status kc_verify(kc_graph* g, const kc_options* opt, kc_mismatch* out, uint64_t cap,
+                    uint64_t* count) {
+  g_last_error.clear();
+  if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
+  if (!count) return fail(KC_ERR_INVALID_ARGUMENT, "count is null");
+  if (cap && !out) return fail(KC_ERR_INVALID_ARGUMENT, "out is null");
+  *count = 0;
+  CK(cudaSetDevice(g->device));
+  if (g->n == 0) return KC_OK;
+  kc_status s = ensure_peel(g);
+  if (s != KC_OK) return s;
+  // candidate: FastK, coreness kept on the device
+  s = kc_solve_device(g, opt, g->d_cand, nullptr);
+  if (s != KC_OK) return s;
+  if (opt && (opt->reserved[0] & KC_DEBUG_VERIFY_PERTURB)) {
+    perturb_kernel<<<g->num_sms, 256, 0, g->stream>>>(g->d_cand, g->n);
+    CK(cudaGetLastError());
+  }
+  s = peel_device(g, nullptr);  // truth into d_out
+  if (s != KC_OK) return s;
+  unsigned long long c = 0;
+  CK(cudaMemsetAsync(g->d_k, 0, sizeof(unsigned long long), g->stream));
+  CK(launch_mismatch_count(g->d_cand, g->d_out, g->n, g->d_k, g->num_sms, g->stream));
+  CK(cudaMemcpyAsync(&c, g->d_k, sizeof(c), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  *count = c;
+  const uint64_t m = c < cap ? c : cap;
+  if (m) {
+    uint32_t* ids = nullptr;
+    kc_mismatch* d_mm = nullptr;
+    CK(dmalloc_n(&ids, m, g->stream));
+    CK(dmalloc_n(&d_mm, m, g->stream));
+    CK(launch_mismatch_list(g->d_cand, g->d_out, g->n, ids, (uint32_t)m, g->stream));
+    mismatch_gather_kernel<<<g->num_sms, 256, 0, g->stream>>>(ids, (uint32_t)m, g->d_cand,
+                                                             g->d_out, d_mm);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, d_mm, m * sizeof(kc_mismatch), cudaMemcpyDeviceToHost, g->stream));
+    dfree(ids, g->stream);
+    dfree(d_mm, g->stream);
+    CK(cudaStreamSynchronize(g->stream));
+  }
   return KC_OK;
 }
 

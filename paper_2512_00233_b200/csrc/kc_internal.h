@@ -128,6 +128,27 @@ inline cudaError_t dmalloc_n(T** p, size_t count, cudaStream_t s) {
   return dmalloc(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T), s);
 }
 
+// Independent device peel + verify (kc_peel.cu).
+struct PeelBuffers {
+  const void* off;           // layout offsets (uint32 or uint64)
+  const uint32_t* adj;
+  uint32_t n_nz;
+  uint32_t* deg;             // [n_nz] remaining degree
+  uint32_t* core;            // [n_nz] peel level (layout ids)
+  uint32_t* rem[2];          // [n_nz] remaining lists
+  uint32_t* fr[2];           // [n_nz] frontier lists (warp rows)
+  uint32_t* frb[2];          // [n_nz] frontier lists (grid rows)
+  void* ctl;                 // peel_ctl_bytes()
+};
+size_t peel_ctl_bytes();
+cudaError_t launch_peel(const PeelBuffers& b, bool off64, int num_sms, cudaStream_t s);
+cudaError_t launch_peel_out(const PeelBuffers& b, const uint32_t* perm, uint32_t n, uint32_t* out,
+                            int num_sms, cudaStream_t s);
+cudaError_t launch_mismatch_count(const uint32_t* a, const uint32_t* b, uint32_t n,
+                                  unsigned long long* count, int num_sms, cudaStream_t s);
+cudaError_t launch_mismatch_list(const uint32_t* cand, const uint32_t* truth, uint32_t n,
+                                 uint32_t* ids, uint32_t cap, cudaStream_t s);
+
 // On-device layout of an uploaded CSR (kc_prep.cu).
 struct PrepOut {
   void* off;        // OffT [n_nz + 1]
