@@ -22,6 +22,26 @@ namespace {
   throw std::runtime_error(msg);
 }
 
+kc_csr_view view_of(const Graph& g) {
+  kc_csr_view view{};
+  view.n = g.node_count();
+  view.nnz = g.offsets().back();
+  view.offsets = g.offsets().data();
+  view.neighbors = (view.n > 0 && view.nnz > 0) ? g.neighbors(0).data() : nullptr;
+  return view;
+}
+
+// Owns a kc_graph handle for the duration of one call.
+struct Handle {
+  kc_graph* h = nullptr;
+  explicit Handle(const Graph& g, uint32_t flags) {
+    const kc_csr_view view = view_of(g);
+    kc_status s = kc_graph_upload_ex(&view, 0, 0, flags, &h);
+    if (s != KC_OK) raise(s, "kc_graph_upload_ex");
+  }
+  ~Handle() { kc_graph_free(h); }
+};
+
 struct HookCtx {
   RunReport* report;
   const Instrumentation* instr;
@@ -100,6 +120,42 @@ EngineResult fastk_run(const Graph& g, const FastKOptions& opt, const Instrument
   out.result.coreness = std::move(core);
   out.result.k_max = st.k_max;
   out.result.k_avg = st.k_avg;
+  return out;
+}
+
+CorenessResult peel_coreness(const Graph& g) {
+  const uint32_t n = g.node_count();
+  std::vector<uint32_t> core(n);
+  if (n == 0) return make_coreness_result(std::move(core));
+  Handle h(g, KC_UPLOAD_UNSORTED_ROWS);
+  kc_stats st{};
+  kc_status s = kc_peel(h.h, core.data(), &st);
+  if (s != KC_OK) raise(s, "kc_peel");
+  return make_coreness_result(std::move(core));
+}
+
+std::vector<Mismatch> verify_fastk(const Graph& g, const FastKOptions& opt, Rule rule) {
+  if (opt.threads == 0) throw std::invalid_argument("fastk: threads must be >= 1");
+  if (opt.batch == 0) throw std::invalid_argument("fastk: batch must be >= 1");
+  std::vector<Mismatch> out;
+  if (g.node_count() == 0) return out;
+  kc_options o;
+  kc_default_options(&o);
+  o.threads = opt.threads;
+  o.batch = opt.batch;
+  o.extended_notify = opt.extended_notify ? 1 : 0;
+  o.hybrid_tail = opt.hybrid_tail ? 1 : 0;
+  o.rule = static_cast<int32_t>(rule);
+  Handle h(g, 0);
+  uint64_t count = 0;
+  std::vector<kc_mismatch> mm(1024);
+  kc_status s = kc_verify(h.h, &o, mm.data(), mm.size(), &count);
+  if (s == KC_OK && count > mm.size()) {
+    mm.resize(count);
+    s = kc_verify(h.h, &o, mm.data(), mm.size(), &count);
+  }
+  if (s != KC_OK) raise(s, "kc_verify");
+  for (uint64_t i = 0; i < count; ++i) out.push_back({mm[i].node, mm[i].candidate, mm[i].truth});
   return out;
 }
 

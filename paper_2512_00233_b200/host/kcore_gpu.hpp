@@ -14,8 +14,11 @@
 // headers — it is the file a maintainer adds to the reference build.
 #pragma once
 
+#include <vector>
+
 #include "kcore/fastk.hpp"
 #include "kcore/graph.hpp"
+#include "kcore/oracle.hpp"
 #include "kcore/report.hpp"
 
 namespace kcore::gpu {
@@ -26,5 +29,15 @@ enum class Rule { Reference = 0, Counting = 1, Auto = 2 };
 
 EngineResult fastk_run(const Graph& g, const FastKOptions& options = {},
                        const Instrumentation* instr = nullptr, Rule rule = Rule::Auto);
+
+// kcore::peel_coreness (include/kcore/oracle.hpp:19-22) computed on the B200
+// by an independent algorithm (kc_peel: level-synchronous parallel peel).
+CorenessResult peel_coreness(const Graph& g);
+
+// kcore::verify(fastk_run(g, options), peel_coreness(g)) (oracle.hpp:29-31)
+// with both results and the comparison on the device: only mismatches
+// (ascending node id) come back.
+std::vector<Mismatch> verify_fastk(const Graph& g, const FastKOptions& options = {},
+                                   Rule rule = Rule::Auto);
 
 }  // namespace kcore::gpu

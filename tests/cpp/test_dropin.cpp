@@ -161,6 +161,19 @@ int main() {
       for (uint32_t b : {1u, 64u, 256u, 4096u})
         CHECK(gpu::fastk_run(g, opts(t, b)).result.coreness == base.result.coreness);
   }
+  {  // the independent device peel and device verify vs the reference peel
+    std::mt19937_64 rng(77);
+    for (int i = 0; i < 40; ++i) {
+      Graph g = gnp(rng, 20 + 7 * i, 0.02 + 0.01 * (i % 9));
+      const CorenessResult want = peel_coreness(g);
+      const CorenessResult got = gpu::peel_coreness(g);
+      CHECK(got.coreness == want.coreness);
+      CHECK(got.k_max == want.k_max && got.k_avg == want.k_avg);
+      CHECK(gpu::verify_fastk(g).empty());
+      CHECK(gpu::verify_fastk(g, opts(4, 8), R).empty());
+    }
+    CHECK(gpu::peel_coreness(Graph()).coreness.empty());
+  }
   std::printf("test_dropin: %d checks, %d failed\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
