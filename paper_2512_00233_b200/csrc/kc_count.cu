@@ -1496,6 +1496,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
   __shared__ uint32_t s_wn[NWARPS][NCLS];
   __shared__ FlatW s_flat[(KC_FLAT_EVAL || KC_FLAT_NOTIFY) ? NWARPS : 1];
   __shared__ Shared sh;
+  __shared__ uint32_t s_qcnt[NCLS];
   uint32_t* wn = s_wn[warp_id()];
   const uint32_t tid = threadIdx.x;
   Enq q;
@@ -1511,7 +1512,11 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     View<EstT> v;
     v.snap = p.E;
     v.q = r == 0 ? nullptr : p.queue[cur];
-    v.qcnt = p.ctl[cur].qcnt;
+    // this round's class sizes, final since the last grid barrier: one
+    // global read per CTA, then shared memory for every grab loop
+    if (tid < NCLS) s_qcnt[tid] = p.ctl[cur].qcnt[tid];
+    __syncthreads();
+    v.qcnt = s_qcnt;
     v.grab = p.ctl[cur].grab;
     v.qn = p.ctl[nxt].qcnt;
     v.qnext = p.queue[nxt];
