@@ -689,6 +689,8 @@ struct FlatW {                // per-warp batch state (shared memory)
   uint32_t lo[32];            // evaluate: window floor L; notify: t (new estimate)
   uint32_t list[32];          // segment reads radj (1) or adj (0)
   unsigned long long ob[32];  // segment start in adj / radj
+  uint32_t above[32];         // notify: count(N >= t) per segment (next-round evaluation)
+  uint32_t slo[32];           // notify: floor of the segment's next-round window
 };
 
 __device__ __forceinline__ uint32_t flat_fb(uint32_t G) {  // bins per vertex
@@ -1278,17 +1280,39 @@ __device__ __forceinline__ void flat_notify_impl(const CP<OffT, EstT>& p, const 
     __syncwarp();
     if (n < 32 && lane == 0) fw.pre[n] = fw.pre[32];
     __syncwarp();
+    // next-round evaluation of each listed dropper (as notify_warp's spec):
+    // values >= t counted, the FB levels below t binned, floor = the list
+    // threshold (levels below it are not decided by the list)
+    const uint32_t FB = flat_fb(grab_size(v.qcnt[c], gmax));
+    {
+      const uint32_t sl = d.t > FB ? d.t - FB : 1u;
+      fw.slo[lane] = d.thr > sl ? d.thr : sl;
+      fw.above[lane] = 0;
+      for (uint32_t i = lane; i < (uint32_t)WARP_BINS; i += 32) bins[i] = 0;
+    }
+    __syncwarp();
     nscan += len;
     flat_stream(p, fw, n, (const EstT*)p.N, s_cache, cache_n,
                 [&](const uint32_t(&seg)[8], const uint32_t(&ids)[8], const uint32_t(&x)[8],
                     uint32_t ok) {
                   uint32_t fire = 0;
+                  uint32_t cs = seg[0], cc = 0;  // run of this lane's entries in one segment
 #pragma unroll
                   for (int j = 0; j < 8; ++j) {
                     const uint32_t sj = seg[j];
-                    const bool f = (ok >> j & 1) && fw.lo[sj] < x[j] && x[j] <= fw.hi[sj];
+                    const uint32_t tj = fw.lo[sj];
+                    const bool v = ok >> j & 1;
+                    const bool f = v && tj < x[j] && x[j] <= fw.hi[sj];
                     fire |= (uint32_t)f << j;
+                    if (sj != cs) {
+                      if (cc) atomicAdd(&fw.above[cs], cc);
+                      cs = sj;
+                      cc = 0;
+                    }
+                    if (v && x[j] >= tj) ++cc;
+                    else if (v && x[j] >= fw.slo[sj]) atomicAdd(&bins[sj * FB + (tj - 1 - x[j])], 1u);
                   }
+                  if (cc) atomicAdd(&fw.above[cs], cc);
                   uint32_t act = 0;
                   if (fire) {
                     fires += __popc(fire);
@@ -1305,6 +1329,25 @@ __device__ __forceinline__ void flat_notify_impl(const CP<OffT, EstT>& p, const 
                       if (__any_sync(FULL, act >> j & 1)) wq_push(p, q, (act >> j & 1) != 0, ids[j]);
                   }
                 });
+    __syncwarp();
+    if (KC_SPEC && flat) {  // lane = segment: resolve the window (kernel.hpp:36-41)
+      const uint32_t C = fw.above[lane];
+      uint32_t lvl = d.t, run = C;
+      bool found = C >= d.t;  // no drop next round
+      for (uint32_t k = 0; !found && k < FB && d.t - 1 - k >= fw.slo[lane]; ++k) {
+        run += bins[lane * FB + k];
+        if (run >= d.t - 1 - k) {
+          lvl = d.t - 1 - k;
+          found = true;
+        }
+      }
+      if (found) {
+        p.spec_t[d.u] = lvl;
+        p.spec_c[d.u] = run;
+        p.spec_r[d.u] = v.round + 1;
+      }
+    }
+    __syncwarp();
     if (flat) p.E[d.u] = (EstT)d.t;  // apply (fastk.cpp:153)
     // droppers without a list: per-vertex pass that builds it
     uint32_t rest = __ballot_sync(FULL, lane < n && !flat);

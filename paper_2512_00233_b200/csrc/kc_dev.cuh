@@ -97,9 +97,32 @@ struct Vals<uint32_t, R> {
 // RO: the array is immutable for the kernel's lifetime (the CSR) — non-
 // coherent path, no L1 allocation (L1 is left to the estimate gathers).
 // Otherwise (lists rewritten inside the kernel): L2 only.
+// The id streams are read once per phase: with KC_L2_STREAM_FIRST (default) they carry
+// an L2 evict-first policy so they do not push the gathered estimates out of
+// L2 (the estimates of R-MAT 26 alone are 134 MB): -2.4% on R-MAT 22, -2.2% on R-MAT 26.
+#ifndef KC_L2_STREAM_FIRST
+#define KC_L2_STREAM_FIRST 1
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 template <bool RO>
 __device__ __forceinline__ uint4 ld_ids4(const uint32_t* src, uint64_t a) {
   uint4 r;
+#if KC_L2_STREAM_FIRST
+  const uint64_t pol = l2_evict_first_policy();
+  if (RO)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(src + a), "l"(pol));
+  else
+    asm volatile("ld.global.cg.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(src + a), "l"(pol));
+#else
   if (RO)
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
@@ -108,6 +131,7 @@ __device__ __forceinline__ uint4 ld_ids4(const uint32_t* src, uint64_t a) {
     asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(src + a));
+#endif
   return r;
 }
 __device__ __forceinline__ uint32_t u4_get(const uint4& q, int e) {
