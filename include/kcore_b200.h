@@ -44,8 +44,9 @@ typedef enum kc_status {
 typedef enum kc_rule {
   /* fastk_run's rule: droppers notify neighbours with extended_notify judged
    * on SETTLED estimates (fastk.cpp:156-163); notified vertices are
-   * re-evaluated.  With hybrid_tail = 0 the RunReport counters equal the
-   * reference's. */
+   * re-evaluated.  The RunReport counters (iterations, messages_sent,
+   * messages_drained, tail_pops) equal the reference's, with or without
+   * hybrid_tail (kc_tail.cu runs the reference's sequential tail). */
   KC_RULE_REFERENCE = 0,
   /* support counters: cnt[v] = #{w in N(v) : est_w >= est_v}; a drop of u
    * across est_w (the extended rule on settled values) decrements cnt[w], and
@@ -60,7 +61,8 @@ typedef struct kc_options {
   uint32_t threads;        /* validated >= 1 like the reference; advisory on GPU */
   uint32_t batch;          /* validated >= 1; hybrid switch threshold (fastk.hpp:29-31) */
   int32_t extended_notify; /* fastk.hpp:18 */
-  int32_t hybrid_tail;     /* fastk.hpp:21: small-frontier single-CTA rounds */
+  int32_t hybrid_tail;     /* fastk.hpp:21: KC_RULE_REFERENCE finishes with the sequential
+                              tail once fewer than `batch` vertices are active */
   int32_t rule;            /* kc_rule */
   uint32_t max_rounds;     /* 0 = default safety cap */
   uint32_t smem_cache;     /* ids whose estimates are cached in shared memory per
@@ -77,11 +79,11 @@ typedef struct kc_stats {
   uint64_t iterations;       /* executed rounds incl. the final quiescent one */
   uint64_t messages_sent;    /* notifications fired */
   uint64_t messages_drained; /* vertex evaluations (incl. isolated vertices in round 0) */
-  uint64_t tail_pops;        /* evaluations done in the single-CTA tail mode */
+  uint64_t tail_pops;        /* queue pops of the sequential tail (fastk.cpp:28-55) */
   uint64_t e_scan;           /* adjacency entries scanned by evaluations */
   uint64_t v_eval;           /* evaluations of non-isolated vertices */
   uint64_t drops;            /* estimate decreases */
-  uint64_t tail_rounds;      /* rounds run in the single-CTA tail mode */
+  uint64_t tail_rounds;      /* 1 if the sequential tail ran */
   uint32_t k_max;            /* CorenessResult::k_max (oracle.hpp:12) */
   uint32_t h_graph;          /* h-index of the degree sequence */
   double k_avg;              /* CorenessResult::k_avg (oracle.hpp:13) */
