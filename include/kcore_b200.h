@@ -35,7 +35,9 @@ typedef enum kc_status {
   KC_ERR_OUT_OF_MEMORY = 3,    /* reference: std::bad_alloc */
   KC_ERR_CUDA = 4,             /* any other CUDA runtime error */
   KC_ERR_NOT_CONVERGED = 5,    /* round cap exceeded (never expected) */
-  KC_ERR_CALLBACK = 6          /* an inspector callback asked to stop */
+  KC_ERR_CALLBACK = 6,         /* an inspector callback asked to stop */
+  KC_ERR_PARSE = 7,            /* reference: kcore::ParseError (graph.hpp:13-23) */
+  KC_ERR_IO = 8                /* reference: kcore::IoError (graph.hpp:25-28) */
 } kc_status;
 
 /* Which vertices a round re-evaluates.  Every rule follows
@@ -217,10 +219,33 @@ kc_status kc_debug_round_stats(kc_graph* g, unsigned long long* out, uint32_t ro
 typedef struct kc_csr_dev {
   kc_csr_view view; /* device pointers */
   int device;
+  const uint64_t* original_ids; /* DEVICE, n entries: dense id -> source id
+                                   (Graph::original_id, graph.hpp:57); NULL =
+                                   identity (generated graphs) */
 } kc_csr_dev;
 kc_status kc_gen_config(int cfg, uint64_t p0, uint64_t p1, uint64_t p2, uint64_t seed,
                         int device, kc_csr_dev** out);
 void kc_csr_dev_free(kc_csr_dev* g);
+/* ---- edge-list ingest ------------------------------ */
+/* kcore::load_edge_list (graph.hpp:76-84, graph.cpp:22-80, 141-199) on the
+ * device: "u v" per line, '#' comments and blank lines skipped, ids are
+ * arbitrary unsigned 64-bit and densified to the ranks of the ascending
+ * distinct ids, self-loops dropped, duplicates collapsed, rows sorted.
+ * `text` is HOST memory.  On malformed input returns KC_ERR_PARSE and fills
+ * *err (may be NULL) with the 1-based line and the reference's message. */
+typedef struct kc_parse_error {
+  uint64_t line;
+  char what[160];
+} kc_parse_error;
+kc_status kc_load_edge_list(const char* text, uint64_t len, int device, kc_csr_dev** out,
+                            kc_parse_error* err);
+/* Same from a plain-text file (gzip input is out of scope: no zlib in the
+ * product); KC_ERR_IO if it cannot be read. */
+kc_status kc_load_edge_list_file(const char* path, int device, kc_csr_dev** out,
+                                 kc_parse_error* err);
+/* Host copy of the original ids of a device CSR (n entries). */
+kc_status kc_csr_dev_original_ids(const kc_csr_dev* g, uint64_t* ids);
+
 /* Copy a device CSR to host buffers (offsets n+1, neighbours nnz). */
 kc_status kc_csr_dev_download(const kc_csr_dev* g, uint64_t* offsets, uint32_t* neighbors);
 

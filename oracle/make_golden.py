@@ -195,6 +195,58 @@ def make_configs(which):
             json.dump(have, f, indent=1)
 
 
+def edge_list_cases():
+    """Texts exercising kcore::load_edge_list (graph.cpp:22-80, 141-199)."""
+    rng = np.random.default_rng(2024)
+    cases = {
+        "basic": "# comment\n10 20\n20 30\n 30\t10 \r\n\n5 5\n",
+        "crlf_no_final_newline": "1 2\r\n2 3\r\n3 1",
+        "dups_loops_reversed": "4 4\n1 2\n2 1\n1 2\n2 3\n3 3\n",
+        "sparse_large_ids": "18446744073709551615 0\n1099511627776 7\n7 18446744073709551615\n",
+        "leading_zeros_tabs": "\t0001\t\t002\n002 \t 3\r\n",
+        "empty": "",
+        "only_comments": "# a\n   # b\n\n\t\r\n",
+        "err_token": "1 2\n3 x4\n5 6\n",
+        "err_negative": "-1 2\n",
+        "err_plus": "1 2\n+3 4\n",
+        "err_overflow": "18446744073709551616 1\n",
+        "err_one_id": "1 2\n\n7\n",
+        "err_three_ids": "1 2\n2 3 4\n",
+        "err_trailing_comment": "1 2 # c\n",
+        "err_last_line_no_newline": "1 2\n3",
+        "err_first_of_two": "a b\n1\n",
+        "err_vertical_tab": "1\v2\n",
+    }
+    lines = []
+    for _ in range(3000):  # random spacing, comments, large and small ids
+        r = rng.random()
+        if r < 0.05:
+            lines.append("# " + "x" * int(rng.integers(0, 10)))
+        elif r < 0.08:
+            lines.append(" \t" * int(rng.integers(0, 3)))
+        else:
+            a = int(rng.integers(0, 500)) if rng.random() < 0.7 else int(rng.integers(0, 2**63))
+            b = int(rng.integers(0, 500)) if rng.random() < 0.7 else int(rng.integers(0, 2**63))
+            sep = [" ", "\t", "  ", " \t "][int(rng.integers(0, 4))]
+            lines.append(f"{a}{sep}{b}" + ("\r" if rng.random() < 0.1 else ""))
+    cases["random_3000"] = "\n".join(lines) + "\n"
+    return cases
+
+
+def make_edge_lists():
+    out = {}
+    for name, text in edge_list_cases().items():
+        try:
+            g, ids = O.ref_load_edge_list(text.encode())
+            out[name] = {"text": text, "n": g.n, "offsets": g.off.tolist(),
+                         "neighbors": g.nbr.tolist(), "original_ids": [str(int(x)) for x in ids]}
+        except ValueError as e:
+            out[name] = {"text": text, "error_line": e.line, "error": str(e)}
+        print(name, {k: v for k, v in out[name].items() if k in ("n", "error")}, flush=True)
+    with open(os.path.join(GOLDEN, "edge_lists.json"), "w") as f:
+        json.dump(out, f, indent=0)
+
+
 def add_ref_counters(which):
     """RunReport of the unmodified reference kcore::fastk_run with its
     defaults (batch 256, extended notify, hybrid tail) on the full-size
@@ -219,6 +271,7 @@ if __name__ == "__main__":
     ap.add_argument("--configs", default="", help="comma list of config ids to digest")
     ap.add_argument("--no-small", action="store_true")
     ap.add_argument("--ref-counters", default="", help="comma list: add the reference's RunReport")
+    ap.add_argument("--edge-lists", action="store_true", help="edge-list loader fixtures")
     a = ap.parse_args()
     O.build(ref=True)
     if not a.no_small:
@@ -227,3 +280,5 @@ if __name__ == "__main__":
         make_configs([int(x) for x in a.configs.split(",")])
     if a.ref_counters:
         add_ref_counters([int(x) for x in a.ref_counters.split(",")])
+    if a.edge_lists:
+        make_edge_lists()

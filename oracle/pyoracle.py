@@ -111,6 +111,12 @@ def ref():
         L.ref_graph_from_edges.restype = C.c_void_p
         L.ref_graph_from_edges.argtypes = [C.c_uint32, _u32p, C.c_uint64]
         L.ref_graph_free.argtypes = [C.c_void_p]
+        L.ref_load_edge_list.restype = C.c_void_p
+        L.ref_load_edge_list.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64,
+                                         C.POINTER(C.c_uint64)]
+        L.ref_graph_n.restype = C.c_uint32
+        L.ref_graph_n.argtypes = [C.c_void_p]
+        L.ref_graph_original_ids.argtypes = [C.c_void_p, _u64p]
         L.ref_graph_nnz.restype = C.c_uint64
         L.ref_graph_nnz.argtypes = [C.c_void_p]
         L.ref_graph_csr.argtypes = [C.c_void_p, _u64p, _u32p]
@@ -290,6 +296,30 @@ def _nbr(g: CSR) -> np.ndarray:
 # --------------------------------------------------------------------------
 # The reference itself (oracle/_ref/libkcore_ref.so)
 # --------------------------------------------------------------------------
+def ref_load_edge_list(text: bytes):
+    """The reference's kcore::load_edge_list on `text` (test infrastructure):
+    returns (CSR, original ids) or raises ValueError("line N: what", line)."""
+    L = ref()
+    err = C.create_string_buffer(512)
+    line = C.c_uint64()
+    h = L.ref_load_edge_list(text, len(text), err, 512, C.byref(line))
+    if not h:
+        e = ValueError(err.value.decode(errors="replace"))
+        e.line = int(line.value)
+        raise e
+    try:
+        n = L.ref_graph_n(h)
+        nnz = L.ref_graph_nnz(h)
+        off = np.zeros(n + 1, dtype=np.uint64)
+        nbr = np.zeros(max(nnz, 1), dtype=np.uint32)
+        L.ref_graph_csr(h, off, nbr)
+        ids = np.zeros(max(n, 1), dtype=np.uint64)
+        L.ref_graph_original_ids(h, ids)
+        return CSR(n, off, nbr[:nnz]), ids[:n]
+    finally:
+        L.ref_graph_free(h)
+
+
 class RefGraph:
     """A kcore::Graph owned by the reference library."""
 

@@ -14,7 +14,9 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "kcore/fastk.hpp"
@@ -80,6 +82,30 @@ void* ref_graph_from_edges(std::uint32_t n, const std::uint32_t* pairs, std::uin
 }
 
 void ref_graph_free(void* g) { delete static_cast<kcore::Graph*>(g); }
+
+// kcore::load_edge_list (graph.cpp:186-199) over an in-memory text.  Returns
+// null on ParseError / IoError with the message in err and the line in *line.
+void* ref_load_edge_list(const char* text, std::uint64_t len, char* err, std::uint64_t errcap,
+                         std::uint64_t* line) {
+  try {
+    std::istringstream in(std::string(text, len));
+    return new kcore::Graph(kcore::load_edge_list(in));
+  } catch (const kcore::ParseError& e) {
+    std::snprintf(err, errcap, "%s", e.what());
+    *line = e.line();
+  } catch (const std::exception& e) {
+    std::snprintf(err, errcap, "%s", e.what());
+    *line = 0;
+  }
+  return nullptr;
+}
+
+std::uint32_t ref_graph_n(const void* g) { return static_cast<const kcore::Graph*>(g)->node_count(); }
+
+void ref_graph_original_ids(const void* gp, std::uint64_t* out) {
+  const auto* g = static_cast<const kcore::Graph*>(gp);
+  for (std::uint32_t u = 0; u < g->node_count(); ++u) out[u] = g->original_id(u);
+}
 
 std::uint64_t ref_graph_nnz(const void* g) {
   return static_cast<const kcore::Graph*>(g)->offsets().back();

@@ -31,7 +31,11 @@ from .api import (  # noqa: F401
     Rule,
     fastk_run,
     fastk_run_abi,
+    IoError,
+    ParseError,
     gen_config,
+    load_edge_list,
+    load_edge_list_file,
     library_path,
     load_library,
     make_coreness_result,

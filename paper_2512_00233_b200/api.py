@@ -50,7 +50,11 @@ class _CSRView(C.Structure):
 
 
 class _CSRDev(C.Structure):
-    _fields_ = [("view", _CSRView), ("device", C.c_int)]
+    _fields_ = [("view", _CSRView), ("device", C.c_int), ("original_ids", C.c_void_p)]
+
+
+class _ParseError(C.Structure):
+    _fields_ = [("line", C.c_uint64), ("what", C.c_char * 160)]
 
 
 _INSPECTOR = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint32), C.c_uint32,
@@ -63,7 +67,8 @@ ABI_SYMBOLS = (
     "kc_graph_nnz", "kc_graph_timings", "kc_solve", "kc_solve_device",
     "kc_solve_observed", "kc_fastk_run", "kc_graph_stream", "kc_gen_config",
     "kc_csr_dev_free", "kc_csr_dev_download", "kc_debug_phase_times", "kc_graph_upload_ex",
-    "kc_debug_round_stats", "kc_solve_traced", "kc_peel", "kc_verify",
+    "kc_debug_round_stats", "kc_solve_traced", "kc_peel", "kc_verify", "kc_load_edge_list",
+    "kc_load_edge_list_file", "kc_csr_dev_original_ids",
 )
 KC_DEBUG_PHASE_TIMES = 1
 KC_DEBUG_LEGACY_COUNT = 2
@@ -121,6 +126,14 @@ def load_library():
     L.kc_solve_traced.argtypes = [C.c_void_p, C.POINTER(_Options), C.c_void_p, C.c_void_p,
                                   C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p,
                                   C.POINTER(_Stats)]
+    L.kc_load_edge_list.restype = C.c_int
+    L.kc_load_edge_list.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.POINTER(C.POINTER(_CSRDev)),
+                                    C.POINTER(_ParseError)]
+    L.kc_load_edge_list_file.restype = C.c_int
+    L.kc_load_edge_list_file.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.POINTER(_CSRDev)),
+                                         C.POINTER(_ParseError)]
+    L.kc_csr_dev_original_ids.restype = C.c_int
+    L.kc_csr_dev_original_ids.argtypes = [C.POINTER(_CSRDev), C.c_void_p]
     L.kc_peel.restype = C.c_int
     L.kc_peel.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Stats)]
     L.kc_verify.restype = C.c_int
@@ -314,8 +327,22 @@ class Graph:
         return v
 
 
+class ParseError(ValueError):
+    """kcore::ParseError (graph.hpp:13-23): malformed edge list, 1-based line."""
+
+    def __init__(self, line: int, what: str):
+        super().__init__(f"line {line}: {what}")
+        self.line = line
+        self.what = what
+
+
+class IoError(RuntimeError):
+    """kcore::IoError (graph.hpp:25-28)."""
+
+
 class DeviceCSR:
-    """A CSR built in HBM by kc_gen_config (synthetic configs, kcgen v1)."""
+    """A CSR in HBM: built by kc_gen_config (synthetic configs, kcgen v1) or
+    loaded from a text edge list (kc_load_edge_list)."""
 
     def __init__(self, ptr):
         self._p = ptr
@@ -338,6 +365,13 @@ class DeviceCSR:
                "kc_csr_dev_download")
         return Graph(off, nbr[: self.nnz])
 
+    def original_ids(self) -> np.ndarray:
+        """Graph::original_id for every dense id (graph.hpp:57)."""
+        ids = np.zeros(max(self.n, 1), dtype=np.uint64)
+        _check(load_library().kc_csr_dev_original_ids(self._p, ids.ctypes.data),
+               "kc_csr_dev_original_ids")
+        return ids[: self.n]
+
     def free(self) -> None:
         if self._p:
             load_library().kc_csr_dev_free(self._p)
@@ -348,6 +382,32 @@ class DeviceCSR:
             self.free()
         except Exception:
             pass
+
+
+def load_edge_list(text, device: int = 0) -> DeviceCSR:
+    """kcore::load_edge_list (graph.hpp:76-81) parsed and densified on the
+    device.  `text`: bytes or str.  Raises ParseError like the reference."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    p = C.POINTER(_CSRDev)()
+    err = _ParseError()
+    st = load_library().kc_load_edge_list(data, len(data), device, C.byref(p), C.byref(err))
+    if st == 7:  # KC_ERR_PARSE
+        raise ParseError(int(err.line), err.what.decode(errors="replace"))
+    _check(st, "kc_load_edge_list")
+    return DeviceCSR(p)
+
+
+def load_edge_list_file(path: str, device: int = 0) -> DeviceCSR:
+    """kcore::load_edge_list_file (graph.hpp:84) for plain-text files."""
+    p = C.POINTER(_CSRDev)()
+    err = _ParseError()
+    st = load_library().kc_load_edge_list_file(path.encode(), device, C.byref(p), C.byref(err))
+    if st == 7:
+        raise ParseError(int(err.line), err.what.decode(errors="replace"))
+    if st == 8:  # KC_ERR_IO
+        raise IoError(err.what.decode(errors="replace"))
+    _check(st, "kc_load_edge_list_file")
+    return DeviceCSR(p)
 
 
 def gen_config(cfg: int, p0: int, p1: int = 0, p2: int = 0, seed: int = 1,

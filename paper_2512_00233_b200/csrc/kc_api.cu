@@ -506,6 +506,8 @@ const char* kc_status_str(kc_status s) {
     case KC_ERR_CUDA: return "CUDA error";
     case KC_ERR_NOT_CONVERGED: return "round cap exceeded before convergence";
     case KC_ERR_CALLBACK: return "inspector callback aborted the run";
+    case KC_ERR_PARSE: return "malformed edge list";
+    case KC_ERR_IO: return "edge list could not be read";
   }
   return "unknown status";
 }

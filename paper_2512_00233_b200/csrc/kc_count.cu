@@ -1540,6 +1540,11 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
   __shared__ FlatW s_flat[(KC_FLAT_EVAL || KC_FLAT_NOTIFY) ? NWARPS : 1];
   __shared__ Shared sh;
   __shared__ uint32_t s_qcnt[NCLS];
+  // the phase's view, published in shared memory: the noinline phase
+  // functions read it through a reference (a stack copy would be local
+  // memory, which misses L1 under this kernel's stack footprint)
+  __shared__ View<EstT> s_view;
+  const View<EstT>& v = s_view;
   uint32_t* wn = s_wn[warp_id()];
   const uint32_t tid = threadIdx.x;
   Enq q;
@@ -1552,28 +1557,28 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
   for (uint32_t r = p.r_begin; r < p.r_end; ++r) {
     const uint32_t cur = r & 1, nxt = cur ^ 1;
     const uint32_t sr = r < STAT_SLOTS - 1 ? r : STAT_SLOTS - 1;
-    View<EstT> v;
-    v.snap = p.E;
-    v.q = r == 0 ? nullptr : p.queue[cur];
+    View<EstT> vl;
+    vl.snap = p.E;
+    vl.q = r == 0 ? nullptr : p.queue[cur];
     // this round's class sizes, final since the last grid barrier: one
     // global read per CTA, then shared memory for every grab loop
     if (tid < NCLS) s_qcnt[tid] = p.ctl[cur].qcnt[tid];
     __syncthreads();
-    v.qcnt = s_qcnt;
-    v.grab = p.ctl[cur].grab;
-    v.qn = p.ctl[nxt].qcnt;
-    v.qnext = p.queue[nxt];
-    q.qn = v.qn;
-    q.qnext = v.qnext;
-    v.r0 = r == 0;
-    v.round = r;
+    vl.qcnt = s_qcnt;
+    vl.grab = p.ctl[cur].grab;
+    vl.qn = p.ctl[nxt].qcnt;
+    vl.qnext = p.queue[nxt];
+    q.qn = vl.qn;
+    q.qnext = vl.qnext;
+    vl.r0 = r == 0;
+    vl.round = r;
     unsigned long long* pf = (p.prof && r < PROF_ROUNDS && tid == 0)
                                  ? p.prof + ((size_t)r * gridDim.x + blockIdx.x) * PROF_PHASES
                                  : nullptr;
     if (pf) pf[0] = gtimer();
     uint32_t active = 0;
 #pragma unroll
-    for (int c = 0; c < NCLS; ++c) active += v.qcnt[c];
+    for (int c = 0; c < NCLS; ++c) active += vl.qcnt[c];
     if (r > 0 && active == 0) {  // quiescent round: converged (fastk.cpp:109-110)
       if (blockIdx.x == 0 && tid == 0) {
         p.status[0] = r + 1;
@@ -1591,15 +1596,16 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
       if (tid < 2) p.ctl[nxt].lqn[tid] = p.ctl[nxt].lqc[tid] = p.ctl[nxt].lqd[tid] = 0;
     }
     if (blockIdx.x == 0 && tid == 32) {
-      p.stats[sr].q01 = v.qcnt[0] | (unsigned long long)v.qcnt[1] << 32;
-      p.stats[sr].q23 = v.qcnt[2] | (unsigned long long)v.qcnt[3] << 32;
-      p.stats[sr].q4 = v.qcnt[4];
+      p.stats[sr].q01 = vl.qcnt[0] | (unsigned long long)vl.qcnt[1] << 32;
+      p.stats[sr].q23 = vl.qcnt[2] | (unsigned long long)vl.qcnt[3] << 32;
+      p.stats[sr].q4 = vl.qcnt[4];
     }
     if (tid < 6) sh.acc[tid] = 0;
     if (tid == 0) sh.drop = 0;
     const uint32_t cache_n = active >= CACHE_MIN_ACTIVE ? p.cache_n : 0u;
-    v.cache_n = cache_n;
+    vl.cache_n = cache_n;
     if (cache_n) fill_cache(s_cache, (const EstT*)p.E, cache_n);
+    if (tid == 0) s_view = vl;
     __syncthreads();
     Acc acc{0, 0, 0, 0, 0, 0, false};
     if (pf) pf[1] = gtimer();
@@ -1648,9 +1654,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     }
     if (pf) pf[5] = gtimer();
     // ---------------- NOTIFY + APPLY ----------------
-    v.snap = p.N;
-    v.grab = p.ctl[cur].grab2;
+    vl.snap = p.N;
+    vl.grab = p.ctl[cur].grab2;
     if (cache_n) fill_cache(s_cache, (const EstT*)p.N, cache_n);
+    if (tid == 0) s_view = vl;
     __syncthreads();
     if (pf) pf[6] = gtimer();
     auto notify_long = [&](uint32_t u) {

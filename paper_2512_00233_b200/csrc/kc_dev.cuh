@@ -105,7 +105,7 @@ struct Vals<uint32_t, R> {
 #endif
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
 

@@ -372,6 +372,14 @@ kc_status build_csr_dev(uint32_t n, const uint2* pairs, uint64_t m, cudaStream_t
 
 }  // namespace
 
+namespace kcb {  // for the edge-list loader (kc_ingest.cu)
+kc_status build_csr_dev_public(uint32_t n, const uint2* pairs, uint64_t m, cudaStream_t s,
+                               uint64_t** off_out, uint32_t** nbr_out, uint64_t* nnz_out) {
+  return build_csr_dev(n, pairs, m, s, off_out, nbr_out, nnz_out);
+}
+const char* gen_last_error() { return g_gen_error.c_str(); }
+}  // namespace kcb
+
 extern "C" {
 
 kc_status kc_gen_config(int cfg, uint64_t p0, uint64_t p1, uint64_t p2, uint64_t seed, int device,
@@ -465,6 +473,7 @@ void kc_csr_dev_free(kc_csr_dev* g) {
   cudaSetDevice(g->device);
   cudaFree(const_cast<uint64_t*>(g->view.offsets));
   cudaFree(const_cast<uint32_t*>(g->view.neighbors));
+  cudaFree(const_cast<uint64_t*>(g->original_ids));
   delete g;
 }
 

@@ -1,6 +1,6 @@
 """Attribute ncu SASS-level stall samples to CUDA source lines.
 
-usage: python scripts/ncu_lines.py <report.ncu-rep> <kernel-substring> [topN] [object]
+usage: python scripts/ncu_lines.py <report.ncu-rep> <kernel-substring> [topN] [object] [function]
 Needs the in-tree build (paper_2512_00233_b200/_build/<object>.o, -lineinfo;
 object defaults to kc_count).
 """
@@ -9,6 +9,7 @@ import collections, csv, io, os, re, subprocess, sys
 rep, kname = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
 objname = sys.argv[4] if len(sys.argv) > 4 else "kc_count"
+only_fn = sys.argv[5] if len(sys.argv) > 5 else None  # e.g. notify_wclass: one subroutine
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
                      capture_output=True, text=True).stdout
@@ -27,11 +28,18 @@ dis = subprocess.run(["nvdisasm", "-g", os.path.join("/tmp", cub[0])], capture_o
                      text=True).stdout
 fn = None
 line = None
+sub = ""
 idx = collections.defaultdict(list)
+subs = collections.defaultdict(list)
 for l in dis.split("\n"):
     m = re.match(r"\s*\.text\.(\S+):", l)
     if m:
         fn = m.group(1)
+        sub = ""
+        continue
+    t = l.strip()
+    if t.startswith("$") and t.endswith(":"):
+        sub = t
         continue
     m = re.search(r'//## File ".*?/([\w.]+)", line (\d+)', l)
     if m:
@@ -39,7 +47,10 @@ for l in dis.split("\n"):
         continue
     if re.match(r"\s+/\*[0-9a-f]{4,}\*/", l) and fn and kname in fn:
         idx[fn].append(line)
-fn_lines = max(idx.values(), key=len) if idx else []
+        subs[fn].append(sub)
+best = max(idx, key=lambda k: len(idx[k])) if idx else None
+fn_lines = idx[best] if best else []
+fn_subs = subs[best] if best else []
 if len(fn_lines) != len(data):
     print(f"warning: {len(fn_lines)} disasm instrs vs {len(data)} profiled", file=sys.stderr)
 agg = collections.Counter()
@@ -48,6 +59,8 @@ agg_stall = collections.defaultdict(collections.Counter)
 tot = 0.0
 for i, r in enumerate(data):
     v = float(r[si] or 0)
+    if only_fn and not (i < len(fn_subs) and only_fn in fn_subs[i]):
+        continue
     tot += v
     key = fn_lines[i] if i < len(fn_lines) else None
     agg[key] += v

@@ -332,3 +332,19 @@ def test_config_digests_reproduce(oracle):
     assert hashlib.sha256(g.nbr.tobytes()).hexdigest() == cfgs["1"]["neighbors_sha256"]
     core = oracle.peel(g)
     assert hashlib.sha256(core.tobytes()).hexdigest() == cfgs["1"]["coreness_sha256"]
+
+
+def test_edge_list_fixtures_match_the_reference(ref):
+    """tests/golden/edge_lists.json is the reference's kcore::load_edge_list
+    output (graph.cpp:22-80, 141-199) — re-derived live when the compiled
+    reference is present."""
+    for name, want in golden("edge_lists.json").items():
+        if "error" in want:
+            with pytest.raises(ValueError) as e:
+                ref.ref_load_edge_list(want["text"].encode())
+            assert str(e.value) == want["error"] and e.value.line == want["error_line"], name
+        else:
+            g, ids = ref.ref_load_edge_list(want["text"].encode())
+            assert g.n == want["n"] and g.off.tolist() == want["offsets"], name
+            assert g.nbr.tolist() == want["neighbors"], name
+            assert [str(int(x)) for x in ids] == want["original_ids"], name
