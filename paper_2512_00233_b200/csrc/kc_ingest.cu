@@ -180,6 +180,12 @@ kc_status ingest(const char* host_text, uint64_t len, int device, kc_csr_dev** o
     err->line = 0;
     err->what[0] = 0;
   }
+  int count = 0;  // no CPU fallback: the loader runs on the device or not at all
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0 || device < 0 || device >= count) {
+    cudaGetLastError();
+    g_ingest_error = "no CUDA device available (the B200 path has no CPU fallback)";
+    return KC_ERR_NO_DEVICE;
+  }
   IK(cudaSetDevice(device));
   cudaStream_t s = 0;
   const int G = 148 * 8, B = 256;

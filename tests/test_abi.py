@@ -51,8 +51,8 @@ def test_library_targets_sm100a_only(kc):
 def test_status_strings_and_defaults(kc):
     L = kc.load_library()
     assert L.kc_abi_version() == 1
-    for s in range(7):
-        assert L.kc_status_str(s)
+    for s in range(9):
+        assert L.kc_status_str(s) and L.kc_status_str(s) != b"unknown status"
     o = kc.api._Options()
     L.kc_default_options(C.byref(o))
     # FastKOptions defaults, include/kcore/fastk.hpp:12-22
@@ -93,3 +93,6 @@ def test_no_cpu_fallback_without_device(kc):
     assert e.value.status == 2  # KC_ERR_NO_DEVICE
     with pytest.raises(kc.KCError):
         kc.gen_config(1, 100, 1000)
+    with pytest.raises(kc.KCError) as e:  # the edge-list loader has no host path either
+        kc.load_edge_list("1 2\n")
+    assert e.value.status == 2
