@@ -186,6 +186,14 @@ typedef struct kc_mismatch {
 kc_status kc_verify(kc_graph* g, const kc_options* opt, kc_mismatch* out, uint64_t cap,
                     uint64_t* count);
 
+/* kcore::sequential_tail (fastk.hpp:38-39, fastk.cpp:28-55) on the device:
+ * est[n] and active[n] (HOST, caller ids) in/out; pops the active vertices
+ * in ascending (estimate, id) order exactly like the reference's min-heap
+ * (kc_tail.cu).  stats: tail_pops, messages_drained, messages_sent of this
+ * call; every flag is 0 on return. */
+kc_status kc_sequential_tail(kc_graph* g, uint32_t* est, uint8_t* active, int extended_notify,
+                             kc_stats* stats);
+
 /* One-shot drop-in: upload (KC_UPLOAD_UNSORTED_ROWS) + solve + download + free
  * (fastk_run semantics). */
 kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* coreness,

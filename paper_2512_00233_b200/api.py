@@ -68,7 +68,7 @@ ABI_SYMBOLS = (
     "kc_solve_observed", "kc_fastk_run", "kc_graph_stream", "kc_gen_config",
     "kc_csr_dev_free", "kc_csr_dev_download", "kc_debug_phase_times", "kc_graph_upload_ex",
     "kc_debug_round_stats", "kc_solve_traced", "kc_peel", "kc_verify", "kc_load_edge_list",
-    "kc_load_edge_list_file", "kc_csr_dev_original_ids",
+    "kc_load_edge_list_file", "kc_csr_dev_original_ids", "kc_sequential_tail",
 )
 KC_DEBUG_PHASE_TIMES = 1
 KC_DEBUG_LEGACY_COUNT = 2
@@ -134,6 +134,8 @@ def load_library():
                                          C.POINTER(_ParseError)]
     L.kc_csr_dev_original_ids.restype = C.c_int
     L.kc_csr_dev_original_ids.argtypes = [C.POINTER(_CSRDev), C.c_void_p]
+    L.kc_sequential_tail.restype = C.c_int
+    L.kc_sequential_tail.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(_Stats)]
     L.kc_peel.restype = C.c_int
     L.kc_peel.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_Stats)]
     L.kc_verify.restype = C.c_int
@@ -510,6 +512,20 @@ class GpuGraph:
                    "kc_solve_traced")
         trace = [IterationStat(float(a), float(b)) for a, b in rows[: nrows.value]]
         return out[: self.n], st.as_dict(), trace
+
+    def sequential_tail(self, est, active, extended_notify: bool = True):
+        """kcore::sequential_tail (fastk.hpp:38-39) on the device: returns
+        (estimates, active flags, stats) — the caller's arrays are not
+        modified."""
+        e = np.ascontiguousarray(est, dtype=np.uint32).copy()
+        a = np.ascontiguousarray(active, dtype=np.uint8).copy()
+        if e.size != self.n or a.size != self.n:
+            raise ValueError("est and active need one entry per vertex")
+        st = _Stats()
+        _check(load_library().kc_sequential_tail(self._h, e.ctypes.data, a.ctypes.data,
+                                                 int(bool(extended_notify)), C.byref(st)),
+               "kc_sequential_tail")
+        return e, a, st.as_dict()
 
     def peel(self):
         """kcore::peel_coreness (oracle.cpp:21-66) as an independent device

@@ -922,6 +922,105 @@ kc_status kc_peel(kc_graph* g, uint32_t* coreness, kc_stats* st) {
   return KC_OK;
 }
 
+// Standalone sequential tail (kcore::sequential_tail, fastk.hpp:38-39): the
+// caller's estimates and active flags (caller ids) in, the device tail, the
+// estimates out.  Isolated vertices never interact: an active one pops once
+// and its estimate becomes 0 (compute_index_over of no values).
+__global__ void tail_in_kernel(const uint32_t* est, const uint8_t* active, const uint32_t* perm,
+                               uint32_t n, uint32_t n_nz, uint32_t* E, uint32_t* N, uint8_t* flag,
+                               uint32_t* est_out, unsigned long long* iso) {
+  unsigned long long c = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t old = perm[i];
+    if (i < n_nz) {
+      E[i] = N[i] = est[old];
+      flag[i] = active[old] != 0;
+    } else {
+      est_out[old] = active[old] ? 0u : est[old];
+      c += active[old] != 0;
+    }
+  }
+  if (c) atomicAdd(iso, c);
+}
+
+__global__ void tail_out_kernel(const uint32_t* E, const uint32_t* perm, uint32_t n_nz,
+                                uint32_t* est_out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_nz; i += gridDim.x * blockDim.x)
+    est_out[perm[i]] = E[i];
+}
+
+kc_status kc_sequential_tail(kc_graph* g, uint32_t* est, uint8_t* active, int extended_notify,
+                             kc_stats* st) {
+  g_last_error.clear();
+  if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
+  if (g->n && (!est || !active)) return fail(KC_ERR_INVALID_ARGUMENT, "est / active is null");
+  if (st) std::memset(st, 0, sizeof(*st));
+  if (g->n == 0) return KC_OK;
+  CK(cudaSetDevice(g->device));
+  kc_status s = ensure_solver(g, 0);
+  if (s != KC_OK) return s;
+  const uint32_t n = g->n, n_nz = g->lay.n_nz;
+  uint32_t *d_est = nullptr, *d_out = nullptr, *E = nullptr, *N = nullptr;
+  uint8_t* d_act = nullptr;
+  unsigned long long* d_iso = nullptr;
+  auto cleanup = [&]() {
+    dfree(d_est, g->stream);
+    dfree(d_out, g->stream);
+    dfree(E, g->stream);
+    dfree(N, g->stream);
+    dfree(d_act, g->stream);
+    dfree(d_iso, g->stream);
+  };
+  cudaError_t e = cudaSuccess;
+  if ((e = dmalloc_n(&d_est, n, g->stream)) != cudaSuccess ||
+      (e = dmalloc_n(&d_out, n, g->stream)) != cudaSuccess ||
+      (e = dmalloc_n(&E, (size_t)n_nz + 16, g->stream)) != cudaSuccess ||
+      (e = dmalloc_n(&N, (size_t)n_nz + 16, g->stream)) != cudaSuccess ||
+      (e = dmalloc_n(&d_act, n, g->stream)) != cudaSuccess ||
+      (e = dmalloc_n(&d_iso, 1, g->stream)) != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "cudaMallocAsync");
+  }
+  unsigned long long iso = 0, tc[TAIL_SLOTS] = {};
+  // 32-bit estimates whatever the handle's width: the caller's values are
+  // arbitrary (fastk.hpp:38-39 takes any est), the tail compares them exactly
+  SolveBuffers b = g->sb;
+  b.est[0] = E;
+  b.est[1] = N;
+  e = cudaMemcpyAsync(d_est, est, (size_t)n * 4, cudaMemcpyHostToDevice, g->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_act, active, n, cudaMemcpyHostToDevice, g->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_iso, 0, 8, g->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(g->sb.tailc, 0, TAIL_SLOTS * 8, g->stream);
+  if (e == cudaSuccess) {
+    tail_in_kernel<<<g->num_sms * 4, 256, 0, g->stream>>>(d_est, d_act, g->lay.perm, n, n_nz, E, N,
+                                                         g->sb.flag[0], d_out, d_iso);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess && n_nz)
+    e = launch_tail(b, g->lay.perm, false, g->lay.off64, extended_notify != 0, 0, g->num_sms,
+                    g->stream);
+  if (e == cudaSuccess) {
+    tail_out_kernel<<<g->num_sms * 4, 256, 0, g->stream>>>(E, g->lay.perm, n_nz, d_out);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(est, d_out, (size_t)n * 4, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&iso, d_iso, 8, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(tc, g->sb.tailc, sizeof(tc), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  cleanup();
+  if (e != cudaSuccess) return cuda_fail(e, "sequential tail");
+  std::memset(active, 0, n);  // every pushed entry was popped: nothing stays active
+  if (st) {
+    st->tail_pops = (n_nz ? tc[TAIL_POPS] : 0) + iso;
+    st->messages_drained = (n_nz ? tc[TAIL_EVALS] : 0) + iso;
+    st->messages_sent = n_nz ? tc[TAIL_FIRES] : 0;
+    st->drops = n_nz ? tc[TAIL_DROPS] : 0;
+    st->e_scan = n_nz ? tc[TAIL_ESCAN] : 0;
+    st->tail_rounds = 1;
+  }
+  return KC_OK;
+}
+
 kc_status kc_verify(kc_graph* g, const kc_options* opt, kc_mismatch* out, uint64_t cap,
                     uint64_t* count) {
   g_last_error.clear();

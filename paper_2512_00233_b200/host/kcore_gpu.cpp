@@ -159,4 +159,20 @@ std::vector<Mismatch> verify_fastk(const Graph& g, const FastKOptions& opt, Rule
   return out;
 }
 
+void sequential_tail(const Graph& g, std::vector<std::uint32_t>& est, ActiveFlags& active,
+                     bool extended_notify, RunReport& report) {
+  const uint32_t n = g.node_count();
+  if (n == 0) return;
+  std::vector<uint8_t> flags(n);
+  for (uint32_t u = 0; u < n; ++u) flags[u] = active[u].load(std::memory_order_relaxed);
+  Handle h(g, KC_UPLOAD_UNSORTED_ROWS);
+  kc_stats st{};
+  kc_status s = kc_sequential_tail(h.h, est.data(), flags.data(), extended_notify ? 1 : 0, &st);
+  if (s != KC_OK) raise(s, "kc_sequential_tail");
+  for (uint32_t u = 0; u < n; ++u) active[u].store(flags[u], std::memory_order_relaxed);
+  report.tail_pops += st.tail_pops;
+  report.messages_drained += st.messages_drained;
+  report.messages_sent += st.messages_sent;
+}
+
 }  // namespace kcore::gpu

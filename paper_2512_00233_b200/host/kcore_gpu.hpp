@@ -30,6 +30,12 @@ enum class Rule { Reference = 0, Counting = 1, Auto = 2 };
 EngineResult fastk_run(const Graph& g, const FastKOptions& options = {},
                        const Instrumentation* instr = nullptr, Rule rule = Rule::Auto);
 
+// kcore::sequential_tail (include/kcore/fastk.hpp:38-39) on the B200: same
+// signature and effect (estimates lowered, flags cleared, pops / drained /
+// sent added to the report).
+void sequential_tail(const Graph& g, std::vector<std::uint32_t>& est, ActiveFlags& active,
+                     bool extended_notify, RunReport& report);
+
 // kcore::peel_coreness (include/kcore/oracle.hpp:19-22) computed on the B200
 // by an independent algorithm (kc_peel: level-synchronous parallel peel).
 CorenessResult peel_coreness(const Graph& g);

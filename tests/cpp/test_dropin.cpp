@@ -174,6 +174,42 @@ int main() {
     }
     CHECK(gpu::peel_coreness(Graph()).coreness.empty());
   }
+  {  // sequential_tail (tests/test_fastk.cpp:318-370): the B200 tail vs the reference's
+    auto flags = [](std::vector<uint8_t> v) {
+      ActiveFlags f(v.size());
+      for (size_t i = 0; i < v.size(); ++i) f[i].store(v[i]);
+      return f;
+    };
+    auto run_both = [&](const Graph& g, std::vector<uint32_t> est, std::vector<uint8_t> act,
+                        bool ext) {
+      std::vector<uint32_t> e1 = est, e2 = est;
+      ActiveFlags a1 = flags(act), a2 = flags(act);
+      RunReport r1, r2;
+      sequential_tail(g, e1, a1, ext, r1);
+      gpu::sequential_tail(g, e2, a2, ext, r2);
+      CHECK(e1 == e2);
+      CHECK(r1.tail_pops == r2.tail_pops);
+      CHECK(r1.messages_drained == r2.messages_drained);
+      CHECK(r1.messages_sent == r2.messages_sent);
+      for (size_t u = 0; u < act.size(); ++u) CHECK(a2[u].load() == 0);
+    };
+    Graph k4p = make(5, {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}, {3, 4}});
+    run_both(k4p, {3, 3, 3, 3, 1}, {1, 1, 1, 1, 1}, true);  // settled: 5 pops, nothing re-entered
+    run_both(k4p, {9, 9, 9, 9, 9}, {0, 0, 0, 0, 0}, true);  // no active node: no-op
+    run_both(make(3, {{0, 1}, {1, 2}}), {1, 2, 2}, {0, 1, 1}, true);  // re-push + stale pop
+    std::mt19937_64 rng(417);
+    for (int rep = 0; rep < 30; ++rep) {
+      Graph g = gnp(rng, 40 + 5 * rep, 0.08);
+      std::vector<uint32_t> est(g.node_count());
+      std::vector<uint8_t> act(g.node_count());
+      std::uniform_int_distribution<uint32_t> big(0, 200000);
+      for (NodeId u = 0; u < g.node_count(); ++u) {
+        est[u] = rep % 3 == 0 ? g.degree(u) : (rep % 3 == 1 ? big(rng) : g.degree(u) / 2);
+        act[u] = (rng() & 3) != 0;
+      }
+      run_both(g, est, act, rep % 2 == 0);
+    }
+  }
   std::printf("test_dropin: %d checks, %d failed\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

@@ -94,3 +94,58 @@ def test_tail_is_invisible_to_the_counting_rule(gpu, oracle):
     b = gpu.fastk_run(G, gpu.FastKOptions(rule=gpu.Rule.COUNTING, hybrid_tail=False))
     assert np.array_equal(a.result.coreness, b.result.coreness)
     assert a.report.tail_pops == 0 and report(a) == report(b)
+
+
+# ---------------------------------------------------- standalone sequential_tail
+def test_standalone_tail_reference_cases(gpu):
+    """tests/test_fastk.cpp:318-357 of the reference, through
+    kc_sequential_tail (fastk.hpp:38-39)."""
+    k4p = gpu.GpuGraph(gpu.Graph.from_edges(5, [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3),
+                                                (2, 3), (3, 4)]))
+    e, a, st = k4p.sequential_tail([3, 3, 3, 3, 1], [1, 1, 1, 1, 1])
+    assert e.tolist() == [3, 3, 3, 3, 1] and a.tolist() == [0] * 5
+    assert (st["tail_pops"], st["messages_drained"], st["messages_sent"]) == (5, 5, 0)
+    e, a, st = k4p.sequential_tail([9] * 5, [0] * 5)
+    assert e.tolist() == [9] * 5 and st["tail_pops"] == 0 and st["messages_drained"] == 0
+    path = gpu.GpuGraph(gpu.Graph.from_edges(3, [(0, 1), (1, 2)]))
+    e, a, st = path.sequential_tail([1, 2, 2], [0, 1, 1])
+    assert e.tolist() == [1, 1, 1]
+    assert (st["tail_pops"], st["messages_drained"], st["messages_sent"]) == (3, 2, 1)
+
+
+def test_standalone_tail_from_degrees_solves(gpu, oracle):
+    # test_fastk.cpp:359-370: the tail alone reaches the coreness from degrees
+    rng = np.random.default_rng(417)
+    for _ in range(10):
+        n = 70
+        iu = np.triu_indices(n, 1)
+        keep = rng.random(iu[0].size) < 0.1
+        g = oracle.build_csr(n, np.stack([iu[0][keep], iu[1][keep]], 1).astype(np.uint32).reshape(-1))
+        gg = gpu.GpuGraph(gpu.Graph(g.off, g.nbr))
+        e, a, _ = gg.sequential_tail(np.diff(g.off).astype(np.uint32), np.ones(n, np.uint8))
+        assert np.array_equal(e, oracle.peel(g)) and not a.any()
+
+
+@pytest.mark.parametrize("ext", [True, False])
+def test_standalone_tail_vs_oracle_and_reference(gpu, oracle, ext):
+    """Arbitrary estimates (above 2^16 too, on a 16-bit handle), random active
+    sets, isolated vertices: estimates and counters equal the C restatement
+    and, where built, the reference's own sequential_tail."""
+    rng = np.random.default_rng(9 + ext)
+    for scale, pairs_fn in ((12, lambda: oracle.gen_rmat(12, 8, 5)),
+                            (0, lambda: oracle.gen_er(3000, 9000, 6))):
+        n = (1 << scale) if scale else 3000
+        g = oracle.build_csr(n, pairs_fn())
+        gg = gpu.GpuGraph(gpu.Graph(g.off, g.nbr))
+        deg = np.diff(g.off).astype(np.uint32)
+        for est in (deg, rng.integers(0, 200000, n).astype(np.uint32), deg // 2):
+            act = (rng.random(n) < 0.6).astype(np.uint8)
+            e, a, st = gg.sequential_tail(est, act, ext)
+            e0, a0, st0 = oracle.sequential_tail(g, est, act, ext)
+            assert np.array_equal(e, e0) and not a.any()
+            for k in ("tail_pops", "messages_drained", "messages_sent"):
+                assert st[k] == st0[k], k
+            if oracle.ref_available():
+                e1, _, st1 = oracle.RefGraph(g).sequential_tail(est, act, ext)
+                assert np.array_equal(e, e1)
+                assert st["tail_pops"] == st1["tail_pops"]
