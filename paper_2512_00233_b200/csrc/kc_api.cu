@@ -447,6 +447,19 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
   }
   uint64_t* d_off = nullptr;
   uint32_t* d_adj = nullptr;
+  // pipelined neighbours (host path): chunks of old rows on a copy stream,
+  // each relabelled by the layout as soon as it lands
+  cudaStream_t cs = nullptr;
+  std::vector<cudaEvent_t> ready;
+  std::vector<uint32_t> old_lo;
+  AdjFeed feed{0, nullptr, nullptr};
+  auto drop_feed = [&]() {
+    for (cudaEvent_t ev : ready)
+      if (ev) cudaEventDestroy(ev);
+    ready.clear();
+    if (cs) cudaStreamDestroy(cs);
+    cs = nullptr;
+  };
   if (!on_device) {
     if (csr->offsets[0] != 0 || csr->offsets[csr->n] != csr->nnz)
       return bail(fail(KC_ERR_INVALID_ARGUMENT, "offsets[0] != 0 or offsets[n] != nnz"));
@@ -459,15 +472,49 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
     }
     e = cudaMemcpyAsync(d_off, csr->offsets, ((size_t)g->n + 1) * sizeof(uint64_t),
                         cudaMemcpyHostToDevice, g->stream);
-    if (e == cudaSuccess && g->nnz)
-      e = cudaMemcpyAsync(d_adj, csr->neighbors, g->nnz * sizeof(uint32_t),
-                          cudaMemcpyHostToDevice, g->stream);
+    // chunks of ~64 MB of neighbours, cut at row boundaries (at most 16)
+    const uint64_t bytes = g->nnz * sizeof(uint32_t);
+    uint64_t k = (bytes + (64ull << 20) - 1) / (64ull << 20);
+    k = k < 1 ? 1 : k > 16 ? 16 : k;
+    old_lo.push_back(0);
+    for (uint64_t c = 1; c < k; ++c) {  // first row whose start is >= c/k of the entries
+      const uint64_t target = g->nnz * c / k;
+      uint32_t lo = old_lo.back(), hi = g->n;
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (csr->offsets[mid] < target) lo = mid + 1; else hi = mid;
+      }
+      if (lo > old_lo.back() && lo < g->n) old_lo.push_back(lo);
+    }
+    old_lo.push_back(g->n);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    cudaEvent_t alloc_done = nullptr;
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(alloc_done, g->stream);  // stream-ordered allocations
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, alloc_done, 0);
+    if (alloc_done) cudaEventDestroy(alloc_done);
+    for (size_t c = 0; e == cudaSuccess && c + 1 < old_lo.size(); ++c) {
+      const uint64_t b0 = csr->offsets[old_lo[c]], b1 = csr->offsets[old_lo[c + 1]];
+      if (b1 > b0)
+        e = cudaMemcpyAsync(d_adj + b0, csr->neighbors + b0, (b1 - b0) * sizeof(uint32_t),
+                            cudaMemcpyHostToDevice, cs);
+      cudaEvent_t ev = nullptr;
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e == cudaSuccess) {
+        ready.push_back(ev);
+        e = cudaEventRecord(ev, cs);
+      }
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(g->ev[1], cs);
     if (e != cudaSuccess) {
+      cudaStreamSynchronize(g->stream);
+      if (cs) cudaStreamSynchronize(cs);
+      drop_feed();
       dfree(d_off, g->stream);
       dfree(d_adj, g->stream);
       return bail(cuda_fail(e, "cudaMemcpy H2D"));
     }
-    cudaEventRecord(g->ev[1], g->stream);
+    feed = AdjFeed{(int)ready.size(), old_lo.data(), ready.data()};
     hc.mark("H2D enqueued");
   } else {
     d_off = const_cast<uint64_t*>(csr->offsets);
@@ -476,10 +523,14 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
     cudaEventRecord(g->ev[1], g->stream);
   }
   e = prep_layout(d_off, d_adj, g->n, g->nnz, (flags & KC_UPLOAD_FORCE_OFF64) != 0,
-                  (flags & KC_UPLOAD_UNSORTED_ROWS) == 0, g->stream, &g->lay);
+                  (flags & KC_UPLOAD_UNSORTED_ROWS) == 0, g->stream, &g->lay,
+                  on_device ? nullptr : &feed);
   hc.mark("layout returned");
+  if (cs) cudaStreamWaitEvent(g->stream, g->ev[1], 0);  // every chunk copied (error paths too)
   cudaEventRecord(g->ev[2], g->stream);
   cudaStreamSynchronize(g->stream);
+  if (cs) cudaStreamSynchronize(cs);
+  drop_feed();
   hc.mark("synced");
   if (!on_device) {
     dfree(d_off, g->stream);

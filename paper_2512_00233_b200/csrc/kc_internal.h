@@ -160,7 +160,16 @@ struct PrepOut {
   uint32_t cls_begin[NCLS + 1];
   bool off64;
 };
+// Pipelined upload (host CSR): the neighbours arrive in k chunks of old row
+// ids [old_lo[c], old_lo[c+1]) (host array, k + 1 entries), chunk c complete
+// when ready[c] fires; the layout relabels each chunk's rows as it lands.
+struct AdjFeed {
+  int k;
+  const uint32_t* old_lo;
+  const cudaEvent_t* ready;
+};
 cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, uint64_t nnz,
-                        bool force_off64, bool sort_rows, cudaStream_t s, PrepOut* out);
+                        bool force_off64, bool sort_rows, cudaStream_t s, PrepOut* out,
+                        const AdjFeed* feed = nullptr);
 
 }  // namespace kcb

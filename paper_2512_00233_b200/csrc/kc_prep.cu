@@ -80,7 +80,8 @@ __global__ void relabel_rows_kernel(const uint64_t* __restrict__ old_off,
                                     const uint32_t* __restrict__ inv,
                                     const uint64_t* __restrict__ chunk_base,  // per row, scan of chunks
                                     uint32_t n_nz, const OffT* __restrict__ new_off,
-                                    uint32_t* __restrict__ new_adj, uint64_t total_chunks) {
+                                    uint32_t* __restrict__ new_adj, uint64_t total_chunks,
+                                    uint32_t o_lo, uint32_t o_hi) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
@@ -92,10 +93,12 @@ __global__ void relabel_rows_kernel(const uint64_t* __restrict__ old_off,
       if (chunk_base[mid] <= c) lo = mid; else hi = mid;
     }
     const uint32_t i = lo;
+    const uint32_t o = perm[i];
+    if (o < o_lo || o >= o_hi) continue;  // pipelined upload: its bytes are not here yet
     const uint64_t k0 = (c - chunk_base[i]) * 1024;
     const uint64_t deg = (uint64_t)(new_off[i + 1] - new_off[i]);
     const uint64_t k1 = k0 + 1024 < deg ? k0 + 1024 : deg;
-    const uint32_t* src = old_adj + old_off[perm[i]];
+    const uint32_t* src = old_adj + old_off[o];
     uint32_t* dst = new_adj + new_off[i];
     for (uint64_t k = k0 + lane; k < k1; k += 32) dst[k] = inv[src[k]];
   }
@@ -109,14 +112,17 @@ __global__ void relabel_small_rows_kernel(const uint64_t* __restrict__ old_off,
                                           const uint32_t* __restrict__ perm,
                                           const uint32_t* __restrict__ inv, uint32_t first,
                                           uint32_t n_nz, const OffT* __restrict__ new_off,
-                                          uint32_t* __restrict__ new_adj) {
+                                          uint32_t* __restrict__ new_adj, uint32_t o_lo,
+                                          uint32_t o_hi) {
   const uint32_t k = threadIdx.x & 7;
   const uint64_t t0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 3;
   const uint64_t nt = (gridDim.x * (uint64_t)blockDim.x) >> 3;
   for (uint64_t i = first + t0; i < n_nz; i += nt) {
+    const uint32_t o = perm[i];
+    if (o < o_lo || o >= o_hi) continue;  // pipelined upload: not here yet
     const uint64_t b = (uint64_t)new_off[i];
     const uint32_t deg = (uint32_t)((uint64_t)new_off[i + 1] - b);
-    const uint32_t* src = old_adj + old_off[perm[i]];
+    const uint32_t* src = old_adj + old_off[o];
     uint32_t v[DEG_SUB_MAX / 8];
 #pragma unroll
     for (int j = 0; j < (int)(DEG_SUB_MAX / 8); ++j) {
@@ -157,7 +163,8 @@ static cudaError_t dalloc(T** p, size_t count, cudaStream_t s) {
 // Relabel + narrow + sort rows.  `off`/`adj` are device pointers to the
 // uploaded reference CSR (not modified).
 cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, uint64_t nnz,
-                        bool force_off64, bool sort_rows, cudaStream_t s, PrepOut* out) {
+                        bool force_off64, bool sort_rows, cudaStream_t s, PrepOut* out,
+                        const AdjFeed* feed) {
   cudaError_t err = cudaSuccess;
   uint32_t *deg = nullptr, *iota = nullptr, *sdeg = nullptr, *perm = nullptr, *inv = nullptr;
   uint32_t* bounds = nullptr;
@@ -232,15 +239,7 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
     // rows of degree > 64 (ids [0, n_big)) are cut into 1024-entry chunks
     // for warps; the rest take the 8-lane-per-row kernel
     const uint32_t n_big = out->cls_begin[C_SUB];
-    if (n_nz > n_big) {
-      if (off64)
-        relabel_small_rows_kernel<uint64_t><<<G, B, 0, s>>>(off, adj, perm, inv, n_big, n_nz,
-                                                            (const uint64_t*)new_off, new_adj);
-      else
-        relabel_small_rows_kernel<uint32_t><<<G, B, 0, s>>>(off, adj, perm, inv, n_big, n_nz,
-                                                            (const uint32_t*)new_off, new_adj);
-      PREP_CK(cudaGetLastError());
-    }
+    uint64_t total = 0;  // 1024-entry chunks of the big rows
     PREP_CK(dalloc(&chunks, (size_t)n_big + 1, s));
     if (n_big) {
       if (off64)
@@ -259,16 +258,39 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
       // chunks[n_big] must be 0 before the exclusive scan so the total lands there
       PREP_CK(cudaMemsetAsync(chunks + n_big, 0, sizeof(uint64_t), s));
       PREP_CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, chunks, chunks, n_big + 1, s));
-      uint64_t total = 0;
       PREP_CK(cudaMemcpyAsync(&total, chunks + n_big, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
       PREP_CK(cudaStreamSynchronize(s));
-      if (off64)
-        relabel_rows_kernel<uint64_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_big,
-                                                      (const uint64_t*)new_off, new_adj, total);
-      else
-        relabel_rows_kernel<uint32_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_big,
-                                                      (const uint32_t*)new_off, new_adj, total);
-      PREP_CK(cudaGetLastError());
+    }
+    // relabel: all rows at once, or — pipelined upload — the rows of each
+    // chunk of old ids as soon as its bytes have landed (event), so the
+    // layout overlaps the host-to-device copy
+    const int nparts = feed ? feed->k : 1;
+    for (int c = 0; c < nparts; ++c) {
+      const uint32_t o_lo = feed ? feed->old_lo[c] : 0u;
+      const uint32_t o_hi = feed ? feed->old_lo[c + 1] : n;
+      if (feed) PREP_CK(cudaStreamWaitEvent(s, feed->ready[c], 0));
+      if (n_nz > n_big) {
+        if (off64)
+          relabel_small_rows_kernel<uint64_t><<<G, B, 0, s>>>(off, adj, perm, inv, n_big, n_nz,
+                                                              (const uint64_t*)new_off, new_adj,
+                                                              o_lo, o_hi);
+        else
+          relabel_small_rows_kernel<uint32_t><<<G, B, 0, s>>>(off, adj, perm, inv, n_big, n_nz,
+                                                              (const uint32_t*)new_off, new_adj,
+                                                              o_lo, o_hi);
+        PREP_CK(cudaGetLastError());
+      }
+      if (n_big) {
+        if (off64)
+          relabel_rows_kernel<uint64_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_big,
+                                                        (const uint64_t*)new_off, new_adj, total,
+                                                        o_lo, o_hi);
+        else
+          relabel_rows_kernel<uint32_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_big,
+                                                        (const uint32_t*)new_off, new_adj, total,
+                                                        o_lo, o_hi);
+        PREP_CK(cudaGetLastError());
+      }
     }
     {
       // sort each row ascending (segmented sort over the new offsets)
