@@ -341,3 +341,20 @@ def test_invalid_arguments_on_device(gpu):
     gg = gpu.GpuGraph(g)
     with pytest.raises(ValueError):
         gg.solve(gpu.FastKOptions(batch=0))
+
+
+def test_repeat_solves_are_stable(gpu):
+    """Races would show up as occasional digest changes: 16 solves of the
+    full R-MAT 22 config under both layouts and both rules."""
+    d = _digests().get("3")
+    if d is None:
+        pytest.skip("golden digest for config 3 not generated")
+    p0, p1, p2, seed = CFG[3]
+    dcsr = gpu.gen_config(3, p0, p1, p2, seed=seed)
+    for flags in (0, gpu.api.KC_UPLOAD_UNSORTED_ROWS):
+        gg = gpu.GpuGraph(dcsr, flags=flags)
+        for r in range(8):
+            rule = gpu.Rule.REFERENCE if r % 4 == 0 else gpu.Rule.COUNTING
+            core, _ = gg.solve(gpu.FastKOptions(rule=rule))
+            assert hashlib.sha256(core.astype(np.uint32).tobytes()).hexdigest() == \
+                d["coreness_sha256"], (flags, r)
