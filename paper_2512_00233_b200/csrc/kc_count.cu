@@ -54,8 +54,17 @@ namespace kcb {
 namespace {
 using namespace dev;
 
-constexpr uint32_t GMAX_BIG = 2, GMAX_WARP = 8, GMAX_SMALL = 32;  // items per grab (max)
-constexpr uint32_t CACHE_MIN_ACTIVE = 4096;  // smaller rounds skip the shared-memory cache
+#ifndef KC_GMAX_BIG
+#define KC_GMAX_BIG 8
+#endif
+#ifndef KC_GMAX_WARP
+#define KC_GMAX_WARP 16
+#endif
+#ifndef KC_CACHE_MIN_ACTIVE
+#define KC_CACHE_MIN_ACTIVE 4096
+#endif
+constexpr uint32_t GMAX_BIG = KC_GMAX_BIG, GMAX_WARP = KC_GMAX_WARP, GMAX_SMALL = 32;  // items per grab (max)
+constexpr uint32_t CACHE_MIN_ACTIVE = KC_CACHE_MIN_ACTIVE;  // smaller rounds skip the shared-memory cache
 #ifndef KC_LIST_MIN_DEG
 #define KC_LIST_MIN_DEG 64
 #endif
