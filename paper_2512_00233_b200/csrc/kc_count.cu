@@ -63,13 +63,19 @@ using namespace dev;
 #ifndef KC_CACHE_MIN_ACTIVE
 #define KC_CACHE_MIN_ACTIVE 4096
 #endif
-constexpr uint32_t GMAX_BIG = KC_GMAX_BIG, GMAX_WARP = KC_GMAX_WARP, GMAX_SMALL = 32;  // items per grab (max)
+#ifndef KC_GMAX_SMALL
+#define KC_GMAX_SMALL 32
+#endif
+constexpr uint32_t GMAX_BIG = KC_GMAX_BIG, GMAX_WARP = KC_GMAX_WARP, GMAX_SMALL = KC_GMAX_SMALL;  // items per grab (max)
 constexpr uint32_t CACHE_MIN_ACTIVE = KC_CACHE_MIN_ACTIVE;  // smaller rounds skip the shared-memory cache
 #ifndef KC_LIST_MIN_DEG
 #define KC_LIST_MIN_DEG 64
 #endif
 constexpr uint32_t LIST_MIN_DEG = KC_LIST_MIN_DEG;  // rows longer than this keep a list
-constexpr uint32_t WARP_MAX_LEN = DEG_BIG_MAX;  // longest scan a single warp takes
+#ifndef KC_WARP_MAX_LEN
+#define KC_WARP_MAX_LEN DEG_BIG_MAX
+#endif
+constexpr uint32_t WARP_MAX_LEN = KC_WARP_MAX_LEN;  // longest scan a single warp takes
 constexpr int HREG = HIST_BINS > (int)NWARPS * WARP_BINS ? HIST_BINS : (int)NWARPS * WARP_BINS;
 constexpr int WQ = 64;             // per-warp, per-class enqueue buffer (flushed at 32)
 #ifndef KC_FLAT_EVAL
