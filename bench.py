@@ -267,6 +267,7 @@ def run_ours(args, ws, rank, local):
                 "h2d_bytes_per_step": int((n + 1) * 8 + nnz * 4),
                 "device_ms": {k: round(statistics.mean(p[k] for p in parts), 3) for k in parts[0]},
                 "call": "kc_fastk_run (pinned host CSR in, coreness to pinned host memory)",
+                "pinned": bool(off_p.is_pinned() and nbr_p.is_pinned()),
                 "d2h_bytes_per_step": int(n * 4)},
         "gpu_launches": 4 * args.steps,
         "clocks": clk.summary(),

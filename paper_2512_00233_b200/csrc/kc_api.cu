@@ -40,7 +40,14 @@ cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t s) {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
   });
-  return cudaMallocAsync(p, bytes ? bytes : 1, s);
+  static const bool dbg = std::getenv("KC_DEBUG_HOST") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  const cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 1, s);
+  if (dbg) {
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > 0.5) std::fprintf(stderr, "[kc host] dmalloc %zu bytes: %.3f ms\n", bytes, ms);
+  }
+  return e;
 }
 void dfree(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
@@ -219,6 +226,15 @@ void free_solver(kc_graph* g) {
 kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
   (void)max_rounds;
   if (g->solver_ready) return KC_OK;
+  struct Mark {
+    bool on = std::getenv("KC_DEBUG_HOST") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    ~Mark() {
+      if (on)
+        std::fprintf(stderr, "[kc host] ensure_solver allocs %8.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+  } mark;
   const uint32_t n_nz = g->lay.n_nz;
   const size_t es = g->est16 ? 2 : 4;
   const size_t n_pad = (((size_t)n_nz + 15) & ~(size_t)15) + 16;  // 16-byte vectors + slack
@@ -408,7 +424,7 @@ struct HostClock {
   void mark(const char* what) {
     if (!on) return;
     const auto t = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[kc upload] %-22s %8.3f ms\n", what,
+    std::fprintf(stderr, "[kc host] %-22s %8.3f ms\n", what,
                  std::chrono::duration<double, std::milli>(t - t0).count());
   }
 };
@@ -498,6 +514,7 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
       if (b1 > b0)
         e = cudaMemcpyAsync(d_adj + b0, csr->neighbors + b0, (b1 - b0) * sizeof(uint32_t),
                             cudaMemcpyHostToDevice, cs);
+      if (c == 0) hc.mark("H2D chunk 0 enqueued");
       cudaEvent_t ev = nullptr;
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
       if (e == cudaSuccess) {
@@ -599,6 +616,7 @@ kc_status kc_graph_upload_ex(const kc_csr_view* csr, int device, int on_device, 
 
 void kc_graph_free(kc_graph* g) {
   if (!g) return;
+  HostClock hc;
   cudaSetDevice(g->device);
   free_solver(g);
   free_peel(g);
@@ -612,6 +630,7 @@ void kc_graph_free(kc_graph* g) {
     if (ev) cudaEventDestroy(ev);
   if (g->stream) cudaStreamDestroy(g->stream);
   delete g;
+  hc.mark("graph_free");
 }
 
 uint32_t kc_graph_n(const kc_graph* g) { return g ? g->n : 0; }
@@ -653,8 +672,10 @@ static kc_status solve_impl(kc_graph* g, const kc_options* opt, uint32_t* out, b
     }
     return KC_OK;
   }
+  HostClock hc;
   s = ensure_solver(g, o.max_rounds);
   if (s != KC_OK) return s;
+  hc.mark("solve: ensure_solver");
   CK(cudaEventRecord(g->ev[0], g->stream));
   s = init_state(g, o);
   if (s != KC_OK) return s;
@@ -679,6 +700,7 @@ static kc_status solve_impl(kc_graph* g, const kc_options* opt, uint32_t* out, b
     CK(cudaMemcpyAsync(out, g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
   CK(cudaEventRecord(g->ev[3], g->stream));
   CK(cudaStreamSynchronize(g->stream));
+  hc.mark("solve: done");
   if (st) {
     cudaEventElapsedTime(&st->t_solve_ms, g->ev[0], g->ev[1]);
     cudaEventElapsedTime(&st->t_download_ms, g->ev[2], g->ev[3]);
