@@ -87,6 +87,9 @@ constexpr int WQ = 64;             // per-warp, per-class enqueue buffer (flushe
 #ifndef KC_SPEC
 #define KC_SPEC 1                  // notify scans evaluate droppers for the next round
 #endif
+#ifndef KC_SPEC_CTA
+#define KC_SPEC_CTA HIST_BINS      // next-round window of the CTA-wide (hub) notify scans
+#endif
 #ifndef KC_SPEC_BINS
 #define KC_SPEC_BINS 256           // spec window width (levels below t), <= WARP_BINS
 #endif
@@ -1114,7 +1117,9 @@ __device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p, const Enq& 
                                             uint32_t build, uint32_t tag, uint32_t floor) {
   const uint32_t tid = threadIdx.x;
   if (tid == 0) sh.cursor = 0;
-  const uint32_t sl = t > (uint32_t)KC_SPEC_BINS ? t - KC_SPEC_BINS : 1u;
+  // the CTA has HIST_BINS bins: a hub's next-round window reaches that far
+  // below t (hubs drop by more than a warp window early on)
+  const uint32_t sl = t > (uint32_t)KC_SPEC_CTA ? t - KC_SPEC_CTA : 1u;
   const uint32_t slo = floor > sl ? floor : sl;
   if (tag)
     for (int i = tid; i < HIST_BINS; i += SOLVE_THREADS) s_hist[i] = 0;
