@@ -59,7 +59,8 @@ agg_stall = collections.defaultdict(collections.Counter)
 tot = 0.0
 for i, r in enumerate(data):
     v = float(r[si] or 0)
-    if only_fn and not (i < len(fn_subs) and only_fn in fn_subs[i]):
+    if only_fn and not (i < len(fn_subs) and (only_fn in fn_subs[i] if only_fn != "body"
+                                              else fn_subs[i] == "")):
         continue
     tot += v
     key = fn_lines[i] if i < len(fn_lines) else None
