@@ -99,6 +99,9 @@ constexpr int WQ = 64;             // per-warp, per-class enqueue buffer (flushe
 #ifndef KC_LIST_COMPACT
 #define KC_LIST_COMPACT 0          // 1: notify filters lists in place (warp scans)
 #endif
+#ifndef KC_FLAT_META
+#define KC_FLAT_META 1             // per-vertex metadata loaded in one level (see eval_item)
+#endif
 #ifndef KC_R0_LISTS
 #define KC_R0_LISTS 0              // 1: round-0 droppers build their lists in round 0's notify
 #endif
@@ -466,6 +469,31 @@ __device__ __forceinline__ Item eval_item(const CP<OffT, EstT>& p, const View<Es
                                           const EstT* s_cache, uint32_t u) {
   Item it;
   it.u = u;
+#if KC_FLAT_META
+  // every per-vertex field in one level of independent loads (the unused
+  // ones are cheap; a second dependent level per item is not)
+  it.ob = p.off[u];
+  const uint64_t oe = p.off[u + 1];
+  it.cap = est_at(s_cache, v.cache_n, v.snap, u);
+  uint32_t lo = 0, thr = 0, sr = 0, st = 0, sc = 0, rl = 0;
+  if (!v.r0) {
+    lo = p.cnt[u];
+    thr = p.rthr[u];
+    sr = p.spec_r[u];
+    st = p.spec_t[u];
+    sc = p.spec_c[u];
+    rl = p.rlen[u];
+  }
+  it.deg = (uint32_t)(oe - it.ob);
+  it.lo = lo;
+  const bool big = !v.r0 && it.deg > LIST_MIN_DEG;
+  it.thr = big ? thr : 0u;
+  it.list = it.thr != 0;
+  it.spec = big && sr == v.round;
+  it.spec_t = it.spec ? st : 0u;
+  it.spec_c = it.spec ? sc : 0u;
+  it.len = it.spec ? 0u : it.list ? rl : it.deg;
+#else
   it.ob = p.off[u];
   it.deg = (uint32_t)(p.off[u + 1] - it.ob);
   it.cap = est_at(s_cache, v.cache_n, v.snap, u);
@@ -476,6 +504,7 @@ __device__ __forceinline__ Item eval_item(const CP<OffT, EstT>& p, const View<Es
   it.spec_t = it.spec ? p.spec_t[u] : 0u;
   it.spec_c = it.spec ? p.spec_c[u] : 0u;
   it.len = it.spec ? 0u : it.list ? p.rlen[u] : it.deg;
+#endif
   return it;
 }
 
@@ -1215,10 +1244,18 @@ __device__ __forceinline__ Drop drop_item(const CP<OffT, EstT>& p, uint32_t u) {
   d.deg = (uint32_t)(p.off[u + 1] - d.ob);
   d.thr = 0;
   d.len = d.deg;
+#if KC_FLAT_META
+  const uint32_t thr = p.rthr[u], rl = p.rlen[u];  // same level as the loads above
+  if (d.t < d.cap && d.deg > LIST_MIN_DEG && thr) {
+    d.thr = thr;
+    d.len = rl;
+  }
+#else
   if (d.t < d.cap && d.deg > LIST_MIN_DEG) {
     d.thr = p.rthr[u];
     if (d.thr) d.len = p.rlen[u];
   }
+#endif
   return d;
 }
 
