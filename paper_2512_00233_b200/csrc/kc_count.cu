@@ -1448,13 +1448,12 @@ __device__ __forceinline__ void notify_small_impl(const CP<OffT, EstT>& p, const
       const uint32_t u = __shfl_sync(FULL, mu, (int)(i0 + g) & 31);
       uint32_t t = 0, cap = 0, deg = 0;
       uint64_t ob = 0;
-      if (i0 + g < n) {
+      if (i0 + g < n) {  // estimates and offsets in one level of loads
         t = p.N[u];
         cap = p.E[u];
-        if (t < cap) {
-          ob = p.off[u];
-          deg = (uint32_t)(p.off[u + 1] - ob);
-        }
+        ob = p.off[u];
+        deg = (uint32_t)(p.off[u + 1] - ob);
+        if (!(t < cap)) deg = 0;
       }
       uint32_t ids[8], x[8], ok = 0;
 #pragma unroll
