@@ -190,6 +190,39 @@ __device__ __forceinline__ uint32_t grab_size(uint32_t cnt, uint32_t gmax) {
   return per < 1u ? 1u : per > gmax ? gmax : per;
 }
 
+// The warp's next slice [base, base + G) of a class queue (>= cnt: drained).
+// KC_STATIC_FIRST: the first slice is assigned statically — warp w takes
+// slice w, no atomic and no round trip (a small round's whole critical path
+// is a few dependent round trips) — and the atomic cursor hands out the rest,
+// counting past the static range.
+#ifndef KC_STATIC_FIRST
+#define KC_STATIC_FIRST 1
+#endif
+#ifndef KC_STATIC_MAXQ
+#define KC_STATIC_MAXQ 16          // static first slice only for queues <= this many slices per warp
+#endif
+__device__ __forceinline__ uint32_t next_slice(uint32_t* cursor, uint32_t cnt, uint32_t G,
+                                               bool& first) {
+  uint32_t stat = 0;
+  // (big queues: the dynamic grabs balance better, and one round trip per
+  // phase is noise there)
+  if (KC_STATIC_FIRST && cnt <= gridDim.x * NWARPS * G * KC_STATIC_MAXQ) {
+    const uint32_t nw = gridDim.x * NWARPS;
+    if (first) {
+      first = false;
+      const uint32_t b = (blockIdx.x * NWARPS + warp_id()) * G;
+      return b < cnt ? b : cnt;
+    }
+    stat = nw * G;
+    if (stat >= cnt) return cnt;  // the static slices covered the queue
+  }
+  uint32_t base = 0;
+  if (lane_id() == 0)  // plain read first: no atomic once the queue is drained
+    base = *reinterpret_cast<volatile uint32_t*>(cursor) + stat >= cnt ? cnt
+                                                                       : stat + atomicAdd(cursor, G);
+  return __shfl_sync(FULL, base, 0);
+}
+
 // Warp-level queue walk: `proc(u, n)` gets the warp's slice, lane i holding
 // item i (i < n).
 template <typename OffT, typename EstT, typename F>
@@ -200,11 +233,9 @@ __device__ __forceinline__ void for_class(const CP<OffT, EstT>& p, const View<Es
   const uint32_t G = grab_size(cnt, gmax);
   uint32_t* cursor = &v.grab[c];
   const uint32_t lane = lane_id();
+  bool first = true;
   for (;;) {
-    uint32_t base = 0;
-    if (lane == 0)  // plain read first: no atomic once the queue is drained
-      base = *reinterpret_cast<volatile uint32_t*>(cursor) >= cnt ? cnt : atomicAdd(cursor, G);
-    base = __shfl_sync(FULL, base, 0);
+    const uint32_t base = next_slice(cursor, cnt, G, first);
     if (base >= cnt) break;
     const uint32_t n = cnt - base < G ? cnt - base : G;
     uint32_t u = 0;
@@ -618,11 +649,9 @@ __device__ void huge_warps(const CP<OffT, EstT>& p, const View<EstT>& v, Shared&
   const uint32_t cnt = v.qcnt[C_HUGE];
   if (cnt == 0) return;  // CTA- and grid-uniform
   uint32_t* cursor = &v.grab[C_HUGE];
+  bool first = true;
   for (;;) {
-    uint32_t k = 0;
-    if (lane_id() == 0)
-      k = *reinterpret_cast<volatile uint32_t*>(cursor) >= cnt ? cnt : atomicAdd(cursor, 1u);
-    k = __shfl_sync(FULL, k, 0);
+    const uint32_t k = next_slice(cursor, cnt, 1u, first);
     if (k >= cnt) break;
     const uint32_t u = v.q ? v.q[p.cb[C_HUGE] + k] : p.cb[C_HUGE] + k;
     if (is_long(u)) {
@@ -976,8 +1005,9 @@ __device__ __forceinline__ void for_class_lanes(const CP<OffT, EstT>& p, const V
   if (cnt == 0) return;
   const uint32_t G = grab_size(cnt, gmax);
   const uint32_t lane = lane_id();
+  bool first = true;
   for (;;) {
-    const uint32_t base = warp_grab(&v.grab[c], cnt, G);
+    const uint32_t base = next_slice(&v.grab[c], cnt, G, first);
     if (base >= cnt) break;
     const uint32_t n = cnt - base < G ? cnt - base : G;
     for (uint32_t s0 = 0; s0 < n; s0 += 32u * K) {
