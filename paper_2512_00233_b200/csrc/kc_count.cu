@@ -269,6 +269,27 @@ __device__ __noinline__ void wq_flush(const CP<OffT, EstT>& p, const Enq& q, int
   __syncwarp();
 }
 
+// End of the notify phase: every class buffer of the warp flushed with the
+// atomics of all classes in flight together (lane c reserves class c), one
+// round trip instead of one per non-empty class.
+template <typename OffT, typename EstT>
+__device__ __noinline__ void wq_flush_all(const CP<OffT, EstT>& p, const Enq& q) {
+  const uint32_t lane = lane_id();
+  uint32_t n = lane < (uint32_t)NCLS ? q.wn[lane] : 0u;
+  uint32_t base = 0;
+  if (n) base = atomicAdd(&q.qn[lane], n);
+#pragma unroll 1
+  for (int c = 0; c < NCLS; ++c) {
+    const uint32_t nc = __shfl_sync(FULL, n, c);
+    if (!nc) continue;
+    const uint32_t bc = __shfl_sync(FULL, base, c);
+    for (uint32_t i = lane; i < nc; i += 32) q.qnext[p.cb[c] + bc + i] = q.wbuf[c * WQ + i];
+  }
+  __syncwarp();
+  if (lane < (uint32_t)NCLS) q.wn[lane] = 0;
+  __syncwarp();
+}
+
 // One activation per lane at most (a: this lane activates `id`).
 template <typename OffT, typename EstT>
 __device__ __noinline__ void wq_push(const CP<OffT, EstT>& p, const Enq& q, bool a, uint32_t id) {
@@ -1780,8 +1801,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     notify_small(p, v, q, s_cache, C_SUB, acc);
     notify_thread(p, v, q, s_cache, acc);
     consume_long(p, v, sh, ctl, 1, true, notify_long);
-#pragma unroll 1
-    for (int c = 0; c < NCLS; ++c) wq_flush(p, q, c);
+    wq_flush_all(p, q);
     flush_acc(p, sr, acc, sh.acc);
     grid.sync();
     if (pf) pf[7] = gtimer();
