@@ -77,7 +77,10 @@ constexpr uint32_t LIST_MIN_DEG = KC_LIST_MIN_DEG;  // rows longer than this kee
 #endif
 constexpr uint32_t WARP_MAX_LEN = KC_WARP_MAX_LEN;  // longest scan a single warp takes
 constexpr int HREG = HIST_BINS > (int)NWARPS * WARP_BINS ? HIST_BINS : (int)NWARPS * WARP_BINS;
-constexpr int WQ = 64;             // per-warp, per-class enqueue buffer (flushed at 32)
+#ifndef KC_WQ
+#define KC_WQ 64
+#endif
+constexpr int WQ = KC_WQ;          // per-warp, per-class enqueue buffer (flushed at WQ - 32)
 #ifndef KC_FLAT_EVAL
 #define KC_FLAT_EVAL 1             // rounds >= 1: batched flat streams for BIG / WARP evaluate
 #endif
@@ -303,7 +306,7 @@ __device__ __noinline__ void wq_push(const CP<OffT, EstT>& p, const Enq& q, bool
     __syncwarp();
     if (lane_id() == 0) q.wn[cc] = n0 + __popc(m);
     __syncwarp();
-    if (n0 + __popc(m) >= 32) wq_flush(p, q, cc);
+    if (n0 + __popc(m) >= (uint32_t)(WQ - 32)) wq_flush(p, q, cc);
   }
 }
 
