@@ -667,9 +667,9 @@ __device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>&
 // every CTA has finished appending and no ticket is left.
 constexpr uint32_t NONE = 0xffffffffu;
 
-template <typename OffT, typename EstT, typename Long, typename WarpF>
+template <typename OffT, typename EstT, typename WarpF>
 __device__ void huge_warps(const CP<OffT, EstT>& p, const View<EstT>& v, Shared& sh, Ctl& ctl,
-                           int ph, Long&& is_long, WarpF&& warp_fn) {
+                           int ph, WarpF&& warp_fn) {
   const uint32_t cnt = v.qcnt[C_HUGE];
   if (cnt == 0) return;  // CTA- and grid-uniform
   uint32_t* cursor = &v.grab[C_HUGE];
@@ -678,14 +678,12 @@ __device__ void huge_warps(const CP<OffT, EstT>& p, const View<EstT>& v, Shared&
     const uint32_t k = next_slice(cursor, cnt, 1u, first);
     if (k >= cnt) break;
     const uint32_t u = v.q ? v.q[p.cb[C_HUGE] + k] : p.cb[C_HUGE] + k;
-    if (is_long(u)) {
+    if (!warp_fn(u)) {  // too long for a warp: to the CTA-wide queue
       if (lane_id() == 0) {
         const uint32_t slot = atomicAdd(&ctl.lqn[ph], 1u);
         atomicExch(&p.lq[ph][slot], u);
       }
-      continue;
     }
-    warp_fn(u);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1498,17 +1496,26 @@ __device__ __forceinline__ void notify_small_impl(const CP<OffT, EstT>& p, const
   const uint32_t cache_n = v.cache_n;
   uint32_t fires = 0, nscan = 0;
   for_class(p, v, c, GMAX_SMALL, [&](uint32_t mu, uint32_t n) {
+    // the slice's estimates and offsets, one lane per item, in one level of
+    // loads for all of its items (not one round trip per 4-item step)
+    uint32_t mt = 0, mcap = 0, mdeg = 0;
+    uint64_t mob = 0;
+    if (lane_id() < n) {
+      mt = p.N[mu];
+      mcap = p.E[mu];
+      mob = p.off[mu];
+      mdeg = (uint32_t)(p.off[mu + 1] - mob);
+      if (!(mt < mcap)) mdeg = 0;
+    }
     for (uint32_t i0 = 0; i0 < n; i0 += 4) {
-      const uint32_t u = __shfl_sync(FULL, mu, (int)(i0 + g) & 31);
-      uint32_t t = 0, cap = 0, deg = 0;
-      uint64_t ob = 0;
-      if (i0 + g < n) {  // estimates and offsets in one level of loads
-        t = p.N[u];
-        cap = p.E[u];
-        ob = p.off[u];
-        deg = (uint32_t)(p.off[u + 1] - ob);
-        if (!(t < cap)) deg = 0;
-      }
+      const int src = (int)(i0 + g) & 31;
+      const uint32_t u = __shfl_sync(FULL, mu, src);
+      const bool has = i0 + g < n;
+      const uint32_t st = __shfl_sync(FULL, mt, src), scap = __shfl_sync(FULL, mcap, src);
+      const uint32_t sdeg = __shfl_sync(FULL, mdeg, src);
+      const uint64_t sob = __shfl_sync(FULL, mob, src);
+      const uint32_t t = has ? st : 0u, cap = has ? scap : 0u, deg = has ? sdeg : 0u;
+      const uint64_t ob = has ? sob : 0ull;
       uint32_t ids[8], x[8], ok = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -1722,13 +1729,12 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     // ---------------- EVALUATE ----------------
     Ctl& ctl = p.ctl[cur];
     auto eval_long = [&](uint32_t u) { eval_cta(p, v, s_cache, s_hist, sh, u, acc); };
-    huge_warps(
-        p, v, sh, ctl, 0,
-        [&](uint32_t u) { return eval_item(p, v, s_cache, u).len > WARP_MAX_LEN; },
-        [&](uint32_t u) {
-          const Item it = eval_item(p, v, s_cache, u);
-          eval_warp(p, v, s_cache, w_bins, it, acc);
-        });
+    huge_warps(p, v, sh, ctl, 0, [&](uint32_t u) {
+      const Item it = eval_item(p, v, s_cache, u);  // metadata loaded once
+      if (it.len > WARP_MAX_LEN) return false;
+      eval_warp(p, v, s_cache, w_bins, it, acc);
+      return true;
+    });
     consume_long(p, v, sh, ctl, 0, false, eval_long);
     if (pf) pf[2] = gtimer();
     if (v.r0 || !KC_FLAT_EVAL) {
@@ -1780,19 +1786,14 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
       acc.fires += f;
       if (tid == 0) acc.nscan += d.len;
     };
-    huge_warps(
-        p, v, sh, ctl, 1,
-        [&](uint32_t u) {
-          const Drop d = drop_item(p, u);
-          return d.t < d.cap && d.len > WARP_MAX_LEN;
-        },
-        [&](uint32_t u) {
-          const Drop d = drop_item(p, u);
-          if (d.t < d.cap) {
-            acc.fires += notify_drop_warp(p, q, s_cache, cache_n, w_bins, r, d);
-            if (lane_id() == 0) acc.nscan += d.len;
-          }
-        });
+    huge_warps(p, v, sh, ctl, 1, [&](uint32_t u) {
+      const Drop d = drop_item(p, u);  // metadata loaded once
+      if (d.t >= d.cap) return true;   // round 0: evaluated, no drop
+      if (d.len > WARP_MAX_LEN) return false;
+      acc.fires += notify_drop_warp(p, q, s_cache, cache_n, w_bins, r, d);
+      if (lane_id() == 0) acc.nscan += d.len;
+      return true;
+    });
     consume_long(p, v, sh, ctl, 1, false, notify_long);
     if (v.r0 || !KC_FLAT_NOTIFY) {
       notify_wclass(p, v, q, s_cache, w_bins, C_BIG, GMAX_BIG, acc);
