@@ -242,6 +242,8 @@ kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
   std::memset(&b, 0, sizeof(b));
   b.off = g->lay.off;
   b.adj = g->lay.adj;
+  b.dcut = g->lay.dcut;
+  b.dcut_n = g->lay.dcut ? g->lay.max_degree + 2 : 0u;
   b.n_nz = n_nz;
   for (int c = 0; c <= NCLS; ++c) b.cls_begin[c] = g->lay.cls_begin[c];
   g->solver_ready = true;  // so that partial allocations get freed
@@ -625,6 +627,7 @@ void kc_graph_free(kc_graph* g) {
   dfree(g->lay.off, g->stream);
   dfree(g->lay.adj, g->stream);
   dfree(g->lay.perm, g->stream);
+  dfree(g->lay.dcut, g->stream);
   if (g->stream) cudaStreamSynchronize(g->stream);
   for (auto& ev : g->ev)
     if (ev) cudaEventDestroy(ev);

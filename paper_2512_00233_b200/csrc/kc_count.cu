@@ -108,9 +108,37 @@ constexpr int WQ = KC_WQ;          // per-warp, per-class enqueue buffer (flushe
 #ifndef KC_R0_LISTS
 #define KC_R0_LISTS 0              // 1: round-0 droppers build their lists in round 0's notify
 #endif
+#ifndef KC_DCUT
+#define KC_DCUT 1                  // degree cut table on sorted layouts (DegCut)
+#endif
+#ifndef KC_CUT_EVAL
+#define KC_CUT_EVAL 1              // windowed evaluations skip / stop at ids below their floor
+#endif
+#ifndef KC_CUT_NOTIFY
+#define KC_CUT_NOTIFY 0            // notify scans likewise (measured slower: rows 0-1 gain little)
+#endif
+#ifndef KC_CUT_LISTS
+#define KC_CUT_LISTS 1             // ... also on (unsorted) lists: mask only
+#endif
+#ifndef KC_R0_SORTED
+#define KC_R0_SORTED 1             // round 0 on sorted rows without gathers (r0_sorted_warp)
+#endif
 #ifndef KC_LIST_SHIFT
 #define KC_LIST_SHIFT 1            // list threshold L = t - (t >> KC_LIST_SHIFT)
 #endif
+
+// Degree cut table (degree-sorted layouts only).  New ids are assigned in
+// order of non-increasing degree, so cut(x) = #{ids of degree >= x} splits
+// every row: id < cut(x) iff degree >= x.  Estimates never exceed degrees,
+// hence id >= cut(x) implies estimate < x — those entries can be skipped
+// without a gather, and in a row sorted ascending they form its suffix.
+struct DegCut {
+  const uint32_t* t;  // [n]; nullptr: rows not sorted, no cut
+  uint32_t n;         // max degree + 2
+  __device__ __forceinline__ uint32_t at(uint32_t x) const {
+    return !t ? 0xffffffffu : x < n ? t[x] : 0u;
+  }
+};
 
 template <typename OffT, typename EstT>
 struct CP {
@@ -122,6 +150,7 @@ struct CP {
   uint32_t* spec_r;     // speculative next-round evaluation: round it is valid for,
   uint32_t* spec_t;     //   its level and
   uint32_t* spec_c;     //   count(>= level) (computed by the notify scan, see NOTIFY)
+  DegCut dc;
   uint32_t n_nz;
   uint32_t cb[NCLS + 1];
   EstT* E;  // snapshot
@@ -355,7 +384,7 @@ template <typename EstT>
 __device__ __forceinline__ uint2 warp_window(const uint32_t* src, bool ro, const EstT* snap,
                                           const EstT* s_cache, uint32_t cache_n, uint32_t* bins,
                                           uint64_t ob, uint64_t oe, uint32_t cap, uint32_t lo,
-                                          uint32_t deg, bool fine_first) {
+                                          uint32_t deg, bool fine_first, DegCut dc) {
   uint32_t top = cap;
   const uint32_t L0 = lo > 1u ? lo : 1u;
   uint32_t L = L0;
@@ -378,7 +407,7 @@ __device__ __forceinline__ uint2 warp_window(const uint32_t* src, bool ro, const
                            if (x[k] >= top) ++above;
                            else if (x[k] >= L) atomicAdd(&bins[(top - 1 - x[k]) / w], 1u);
                          }
-                       });
+                       }, KC_CUT_EVAL && (KC_CUT_LISTS || ro) ? dc.at(L) : 0xffffffffu, KC_CUT_EVAL && ro && dc.t);
     __syncwarp();
     const uint32_t C = __reduce_add_sync(FULL, above);
     if (top == cap && C >= cap) return make_uint2(cap, C);  // no drop (round 0 only)
@@ -405,7 +434,7 @@ template <typename EstT>
 __device__ __noinline__ void cta_window(const uint32_t* src, bool ro, const EstT* snap, const EstT* s_cache,
                                         uint32_t cache_n, uint32_t* s_hist, uint32_t* s_red,
                                         uint64_t ob, uint64_t oe, uint32_t cap, uint32_t lo,
-                                        uint32_t deg, bool fine_first, uint32_t* out) {
+                                        uint32_t deg, bool fine_first, uint32_t* out, DegCut dc) {
   const uint32_t tid = threadIdx.x;
   uint32_t top = cap;
   const uint32_t L0 = lo > 1u ? lo : 1u;
@@ -430,7 +459,7 @@ __device__ __noinline__ void cta_window(const uint32_t* src, bool ro, const EstT
                                       if (x[k] >= top) ++above;
                                       else if (x[k] >= L) atomicAdd(&s_hist[(top - 1 - x[k]) / w], 1u);
                                     }
-                                  });
+                                  }, KC_CUT_EVAL && (KC_CUT_LISTS || ro) ? dc.at(L) : 0xffffffffu, KC_CUT_EVAL && ro && dc.t);
     const uint32_t C = block_sum(above, s_red);
     if (top == cap && C >= cap) {  // no drop (round 0 only)
       if (tid == 0) {
@@ -580,11 +609,68 @@ __device__ __forceinline__ void finish_eval(const CP<OffT, EstT>& p, const Item&
   if (it.thr != 0 && t < it.thr) p.rthr[it.u] = 0;
 }
 
+// Round 0 on a degree-sorted row (p.dc.t set): the snapshot is E = min(deg,
+// H), non-increasing along the row, so d_i >= i (1-based positions) holds
+// exactly on a prefix and the capped h-index is t = #{i <= cap : row[i-1] <
+// cut(i)}; count(E >= t) = #{j : row[j] < cut(t)}, a prefix of length >= t.
+// Both read the row and the contiguous cut table only — no gathers — and
+// stop at the first position that fails.  Returns (t, count(>= t)).
+template <typename OffT, typename EstT>
+__device__ __forceinline__ uint2 r0_sorted_warp(const CP<OffT, EstT>& p, uint64_t ob, uint32_t deg,
+                                                uint32_t cap, uint32_t& scanned) {
+  const uint32_t lane = lane_id();
+  const uint32_t m = cap < deg ? cap : deg;
+  uint32_t h = 0, i0 = 0;
+  for (; i0 < m; i0 += 256) {
+    uint32_t id[8], ct[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t i = i0 + 32 * k + lane;  // 0-based position
+      id[k] = i < m ? __ldg(p.adj + ob + i) : 0xffffffffu;
+      ct[k] = i < m ? __ldg(p.dc.t + i + 1) : 0u;
+    }
+    bool miss = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool in = i0 + 32 * k + lane < m;
+      h += in && id[k] < ct[k];
+      miss |= in && !(id[k] < ct[k]);
+    }
+    if (__any_sync(FULL, miss)) break;
+  }
+  const uint32_t t = __reduce_add_sync(FULL, h);
+  const uint32_t ctt = __ldg(p.dc.t + t);
+  uint32_t c = 0, j0 = t;
+  for (; j0 < deg; j0 += 256) {
+    uint32_t id[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t j = j0 + 32 * k + lane;
+      id[k] = j < deg ? __ldg(p.adj + ob + j) : 0xffffffffu;
+    }
+    bool miss = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      c += id[k] < ctt;
+      miss |= j0 + 32 * k + lane < deg && !(id[k] < ctt);
+    }
+    if (__any_sync(FULL, miss)) break;
+  }
+  scanned = (i0 < m ? i0 + 256 : m) + (j0 < deg ? j0 + 256 - t : deg - t);
+  return make_uint2(t, t + __reduce_add_sync(FULL, c));
+}
+
 template <typename OffT, typename EstT, typename A>
 __device__ __forceinline__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                           uint32_t* bins, const Item& it, A& acc) {
   if (it.spec) {
     if (lane_id() == 0) finish_eval(p, it, it.spec_t, it.spec_c, 0u, acc);
+    return;
+  }
+  if (KC_R0_SORTED && v.r0 && p.dc.t) {
+    uint32_t scanned = 0;
+    const uint2 tc = r0_sorted_warp(p, it.ob, it.deg, it.cap, scanned);
+    if (lane_id() == 0) finish_eval(p, it, tc.x, tc.y, scanned, acc);
     return;
   }
   const EstT* snap = v.snap;
@@ -606,7 +692,7 @@ __device__ __forceinline__ void eval_warp(const CP<OffT, EstT>& p, const View<Es
     const bool lst = pass == 0;
     const uint32_t len = lst ? it.len : it.deg;
     tc = warp_window(lst ? (const uint32_t*)p.radj : p.adj, !lst, snap, s_cache, cache_n, bins,
-                     it.ob, it.ob + len, it.cap, lst && it.thr > lo ? it.thr : lo, it.deg, !v.r0);
+                     it.ob, it.ob + len, it.cap, lst && it.thr > lo ? it.thr : lo, it.deg, !v.r0, p.dc);
     scanned += len;
     if (tc.x != 0) break;  // found (a list miss falls through to the row)
   }
@@ -644,7 +730,7 @@ __device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>&
   uint32_t scanned = 0;
   if (it.list) {
     cta_window(p.radj, false, snap, s_cache, cache_n, s_hist, sh.red, it.ob, it.ob + it.len,
-                      it.cap, lo > it.thr ? lo : it.thr, it.deg, !v.r0, sh.out);
+                      it.cap, lo > it.thr ? lo : it.thr, it.deg, !v.r0, sh.out, p.dc);
     scanned = it.len;
   } else if (threadIdx.x == 0) {
     sh.out[0] = 0;
@@ -652,7 +738,7 @@ __device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>&
   __syncthreads();
   if (sh.out[0] == 0) {
     cta_window(p.adj, true, snap, s_cache, cache_n, s_hist, sh.red, it.ob, it.ob + it.deg, it.cap,
-                     lo, it.deg, !v.r0, sh.out);
+                     lo, it.deg, !v.r0, sh.out, p.dc);
     scanned += it.deg;
   }
   if (threadIdx.x == 0) finish_eval(p, it, sh.out[0], sh.out[1], scanned, acc);
@@ -1138,6 +1224,10 @@ __device__ __forceinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const E
   uint32_t above = 0;
   const uint32_t sl = t > (uint32_t)KC_SPEC_BINS ? t - KC_SPEC_BINS : 1u;
   const uint32_t slo = floor > sl ? floor : sl;  // spec window [slo, t)
+  // lowest value this scan looks at: t + 1 (notify), slo (spec), build (list)
+  uint32_t need = t + 1;
+  if (tag && slo < need) need = slo;
+  if (build && build < need) need = build;
   if (tag) warp_zero_bins(bins);
   stream_row_rt<32>(src, ro, p.N, lane_id(), ob, ob + len, s_cache, cache_n,
                      [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
@@ -1162,7 +1252,7 @@ __device__ __forceinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const E
                            if (keep >> k & 1) p.radj[ob + pos++] = ids[k];
                          cursor += __shfl_sync(FULL, incl, 31);
                        }
-                     });
+                     }, KC_CUT_NOTIFY && (KC_CUT_LISTS || ro) ? p.dc.at(need) : 0xffffffffu, KC_CUT_NOTIFY && ro && p.dc.t);
   if (tag) {
     __syncwarp();
     const uint32_t C = __reduce_add_sync(FULL, above);
@@ -1202,6 +1292,9 @@ __device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p, const Enq& 
   // below t (hubs drop by more than a warp window early on)
   const uint32_t sl = t > (uint32_t)KC_SPEC_CTA ? t - KC_SPEC_CTA : 1u;
   const uint32_t slo = floor > sl ? floor : sl;
+  uint32_t need = t + 1;  // lowest value this scan looks at (see notify_warp)
+  if (tag && slo < need) need = slo;
+  if (build && build < need) need = build;
   if (tag)
     for (int i = tid; i < HIST_BINS; i += SOLVE_THREADS) s_hist[i] = 0;
   __syncthreads();
@@ -1232,7 +1325,7 @@ __device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p, const Enq& 
                                     for (int k = 0; k < 8; ++k)
                                       if (keep >> k & 1) p.radj[ob + pos++] = ids[k];
                                   }
-                                });
+                                }, KC_CUT_NOTIFY && (KC_CUT_LISTS || ro) ? p.dc.at(need) : 0xffffffffu, KC_CUT_NOTIFY && ro && p.dc.t);
   if (tag) {  // CTA suffix scan of the spec window (one pass, no refinement)
     const uint32_t C = block_sum(above, sh.red);
     constexpr int PER = (HIST_BINS + SOLVE_THREADS - 1) / SOLVE_THREADS;
@@ -1731,7 +1824,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     auto eval_long = [&](uint32_t u) { eval_cta(p, v, s_cache, s_hist, sh, u, acc); };
     huge_warps(p, v, sh, ctl, 0, [&](uint32_t u) {
       const Item it = eval_item(p, v, s_cache, u);  // metadata loaded once
-      if (it.len > WARP_MAX_LEN) return false;
+      // (round 0 on sorted rows reads a prefix only: always a warp's)
+      if (it.len > WARP_MAX_LEN && !(KC_R0_SORTED && v.r0 && p.dc.t)) return false;
       eval_warp(p, v, s_cache, w_bins, it, acc);
       return true;
     });
@@ -1852,6 +1946,8 @@ CP<OffT, EstT> make_params(const SolveBuffers& b) {
   CP<OffT, EstT> p{};
   p.off = static_cast<const OffT*>(b.off);
   p.adj = b.adj;
+  p.dc.t = KC_DCUT ? b.dcut : nullptr;
+  p.dc.n = b.dcut_n;
   p.radj = b.radj;
   p.rlen = b.rlen;
   p.rthr = static_cast<EstT*>(b.rthr);

@@ -327,10 +327,16 @@ __device__ __forceinline__ uint4 ld_ids4_rt(const uint32_t* src, uint64_t a, boo
   return ro ? ld_ids4<true>(src, a) : ld_ids4<false>(src, a);
 }
 
+//
+// `cut`: ids >= cut are masked without a gather (with degree-descending ids,
+// id >= cut(x) means degree < x, so the estimate is < x too).  `stop`: the
+// source is sorted ascending, so once a warp's step holds an id >= cut every
+// later step of that warp does too — the warp leaves the stream.
 template <int NT, typename EstT, typename F>
 __device__ __forceinline__ void stream_row_rt(const uint32_t* src, bool ro, const EstT* snap,
                                               uint32_t me, uint64_t ob, uint64_t oe,
-                                              const EstT* s_cache, uint32_t cache_n, F&& f) {
+                                              const EstT* s_cache, uint32_t cache_n, F&& f,
+                                              uint32_t cut = 0xffffffffu, bool stop = false) {
   constexpr uint64_t STEP = (uint64_t)NT * 8;
   uint64_t a = ob & ~(uint64_t)3;
   uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
@@ -343,15 +349,19 @@ __device__ __forceinline__ void stream_row_rt(const uint32_t* src, bool ro, cons
     if (nb + 4 * me + 4 * NT < oe) n1 = ld_ids4_rt(src, nb + 4 * me + 4 * NT, ro);
     uint32_t ids[8], x[8];
     uint32_t ok = 0;
+    bool past = false;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const uint64_t pos = a + 4 * me + (k >> 2) * 4 * NT + (k & 3);
       ids[k] = u4_get(k < 4 ? q0 : q1, k & 3);
-      const bool v = pos >= ob && pos < oe;
+      const bool in = pos >= ob && pos < oe;
+      const bool v = in && ids[k] < cut;
+      past |= in && !v;
       ok |= (uint32_t)v << k;
       x[k] = v ? est_at(s_cache, cache_n, snap, ids[k]) : 0u;
     }
     f(ok, ids, x);
+    if (stop && __any_sync(FULL, past)) break;
     q0 = n0;
     q1 = n1;
   }
