@@ -1014,14 +1014,17 @@ __device__ __noinline__ void flat_eval(const CP<OffT, EstT>& p, const View<EstT>
 
 // SUB class (deg <= 64): 8-lane tile per vertex, 8 values per lane,
 // bisection on [lo, cap).
+// Round 0 on sorted rows (s_dcut: the cut table's first DEG_SUB_MAX + 2
+// entries in shared memory) takes r0_sorted_warp's rule: no gathers.
 template <typename OffT, typename EstT, typename A>
 __device__ __forceinline__ void eval_sub_impl(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
-                         A& acc) {
+                         const uint32_t* s_dcut, A& acc) {
   constexpr int R = DEG_SUB_MAX / 8;
   const uint32_t g = lane_id() >> 3, k = lane_id() & 7;
   const EstT* snap = v.snap;
   const uint32_t cache_n = v.cache_n;
   const bool r0 = v.r0;
+  const bool r0s = KC_R0_SORTED && r0 && p.dc.t;
   for_class(p, v, C_SUB, GMAX_SMALL, [&](uint32_t mu, uint32_t n) {
     // metadata of the grab, one lane per item, loaded in parallel
     uint64_t mob = 0;
@@ -1052,6 +1055,24 @@ __device__ __forceinline__ void eval_sub_impl(const CP<OffT, EstT>& p, const Vie
           const uint32_t q = k + 8 * j;
           ids[j] = q < deg ? p.adj[ob + q] : 0xffffffffu;
         }
+        if (r0s) {
+          const uint32_t m = deg < cap ? deg : cap;
+          uint32_t hc = 0;
+#pragma unroll
+          for (int j = 0; j < R; ++j) hc += k + 8 * j < m && ids[j] < s_dcut[k + 8 * j + 1];
+          const uint32_t t = tile8_sum(hc);
+          const uint32_t ct = s_dcut[t];
+          uint32_t cc = 0;
+#pragma unroll
+          for (int j = 0; j < R; ++j) cc += ids[j] < ct;
+          const uint32_t c = tile8_sum(cc);
+          if (has && k == 0) {
+            Item it;
+            it.u = u; it.cap = cap; it.deg = deg; it.len = deg; it.thr = 0;
+            finish_eval(p, it, t, t ? c : deg, deg, acc);
+          }
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < R; ++j)
           if (ids[j] != 0xffffffffu) vals.set(j, est_at(s_cache, cache_n, snap, ids[j]));
@@ -1079,9 +1100,9 @@ __device__ __forceinline__ void eval_sub_impl(const CP<OffT, EstT>& p, const Vie
 
 template <typename OffT, typename EstT>
 __device__ __noinline__ void eval_sub(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
-                         Acc& acc) {
+                         const uint32_t* s_dcut, Acc& acc) {
   Acc32 a{0, 0, 0, 0, 0, 0, false};
-  eval_sub_impl(p, v, s_cache, a);
+  eval_sub_impl(p, v, s_cache, s_dcut, a);
   merge_acc(acc, a);
 }
 
@@ -1136,10 +1157,11 @@ __device__ __forceinline__ void for_class_lanes(const CP<OffT, EstT>& p, const V
 
 template <typename OffT, typename EstT, typename A>
 __device__ __forceinline__ void eval_thread_impl(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
-                            A& acc) {
+                            const uint32_t* s_dcut, A& acc) {
   constexpr int R = DEG_THREAD_MAX;
   const EstT* snap = v.snap;
   const uint32_t cache_n = v.cache_n;
+  const bool r0s = KC_R0_SORTED && v.r0 && p.dc.t;
   for_class_lanes<TU>(p, v, C_THREAD, GMAX_THREAD, [&](const uint32_t(&u)[TU], uint32_t valid) {
     uint64_t ob[TU];
     uint32_t deg[TU], cap[TU], x[TU][R];
@@ -1157,6 +1179,24 @@ __device__ __forceinline__ void eval_thread_impl(const CP<OffT, EstT>& p, const 
     for (int k = 0; k < TU; ++k)
 #pragma unroll
       for (int j = 0; j < R; ++j) x[k][j] = (uint32_t)j < deg[k] ? p.adj[ob[k] + j] : 0xffffffffu;
+    if (r0s) {  // round 0, sorted rows: r0_sorted_warp's rule on the ids (no gathers)
+#pragma unroll
+      for (int k = 0; k < TU; ++k) {
+        if (!(valid >> k & 1)) continue;
+        const uint32_t m = deg[k] < cap[k] ? deg[k] : cap[k];
+        uint32_t t = 0;
+#pragma unroll
+        for (int j = 0; j < R; ++j) t += (uint32_t)j < m && x[k][j] < s_dcut[j + 1];
+        const uint32_t ct = s_dcut[t];
+        uint32_t c = 0;
+#pragma unroll
+        for (int j = 0; j < R; ++j) c += x[k][j] < ct;
+        Item it;
+        it.u = u[k]; it.cap = cap[k]; it.deg = deg[k]; it.len = deg[k]; it.thr = 0;
+        finish_eval(p, it, t, t ? c : deg[k], deg[k], acc);
+      }
+      return;
+    }
 #pragma unroll
     for (int k = 0; k < TU; ++k)
 #pragma unroll
@@ -1187,9 +1227,9 @@ __device__ __forceinline__ void eval_thread_impl(const CP<OffT, EstT>& p, const 
 
 template <typename OffT, typename EstT>
 __device__ __noinline__ void eval_thread(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
-                            Acc& acc) {
+                            const uint32_t* s_dcut, Acc& acc) {
   Acc32 a{0, 0, 0, 0, 0, 0, false};
-  eval_thread_impl(p, v, s_cache, a);
+  eval_thread_impl(p, v, s_cache, s_dcut, a);
   merge_acc(acc, a);
 }
 
@@ -1750,6 +1790,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
   __shared__ FlatW s_flat[(KC_FLAT_EVAL || KC_FLAT_NOTIFY) ? NWARPS : 1];
   __shared__ Shared sh;
   __shared__ uint32_t s_qcnt[NCLS];
+  __shared__ uint32_t s_dcut[DEG_SUB_MAX + 2];  // head of the degree cut table (round 0)
   // the phase's view, published in shared memory: the noinline phase
   // functions read it through a reference (a stack copy would be local
   // memory, which misses L1 under this kernel's stack footprint)
@@ -1762,6 +1803,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
   q.wn = wn;
   if (tid == 0) sh.ticket = 0xffffffffu;
   if (lane_id() < NCLS) wn[lane_id()] = 0;
+  if (tid < DEG_SUB_MAX + 2) s_dcut[tid] = p.dc.at(tid);
   __syncthreads();
 
   for (uint32_t r = p.r_begin; r < p.r_end; ++r) {
@@ -1839,8 +1881,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
       flat_eval(p, v, s_cache, w_bins, s_flat[warp_id()], C_WARP, GMAX_WARP, acc);
     }
     if (pf) pf[3] = gtimer();
-    eval_sub(p, v, s_cache, acc);
-    eval_thread(p, v, s_cache, acc);
+    eval_sub(p, v, s_cache, s_dcut, acc);
+    eval_thread(p, v, s_cache, s_dcut, acc);
     consume_long(p, v, sh, ctl, 0, true, eval_long);
     if (pf) pf[4] = gtimer();
     if (v.r0) {
