@@ -1141,6 +1141,9 @@ kc_status kc_verify(kc_graph* g, const kc_options* opt, kc_mismatch* out, uint64
   return KC_OK;
 }
 
+#ifndef KC_ONESHOT_SORT
+#define KC_ONESHOT_SORT 0
+#endif
 kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* coreness,
                        kc_stats* st) {
   kc_options o;
@@ -1148,7 +1151,7 @@ kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* 
   if (s != KC_OK) return s;
   kc_graph* g = nullptr;
   // one solve: the per-row sort of the layout would cost more than it saves
-  s = kc_graph_upload_ex(csr, 0, 0, KC_UPLOAD_UNSORTED_ROWS, &g);
+  s = kc_graph_upload_ex(csr, 0, 0, KC_ONESHOT_SORT ? 0u : KC_UPLOAD_UNSORTED_ROWS, &g);
   if (s != KC_OK) return s;
   s = kc_solve(g, &o, coreness, st);
   kc_graph_free(g);
