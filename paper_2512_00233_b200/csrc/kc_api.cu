@@ -244,6 +244,7 @@ kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
   b.adj = g->lay.adj;
   b.dcut = g->lay.dcut;
   b.dcut_n = g->lay.dcut ? g->lay.max_degree + 2 : 0u;
+  b.rows_sorted = g->lay.rows_sorted;
   b.n_nz = n_nz;
   for (int c = 0; c <= NCLS; ++c) b.cls_begin[c] = g->lay.cls_begin[c];
   g->solver_ready = true;  // so that partial allocations get freed

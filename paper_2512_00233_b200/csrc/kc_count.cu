@@ -133,8 +133,9 @@ constexpr int WQ = KC_WQ;          // per-warp, per-class enqueue buffer (flushe
 // hence id >= cut(x) implies estimate < x — those entries can be skipped
 // without a gather, and in a row sorted ascending they form its suffix.
 struct DegCut {
-  const uint32_t* t;  // [n]; nullptr: rows not sorted, no cut
+  const uint32_t* t;  // [n]; nullptr: no table
   uint32_t n;         // max degree + 2
+  bool sorted;        // rows sorted ascending: prefix rules and early exits apply
   __device__ __forceinline__ uint32_t at(uint32_t x) const {
     return !t ? 0xffffffffu : x < n ? t[x] : 0u;
   }
@@ -407,7 +408,7 @@ __device__ __forceinline__ uint2 warp_window(const uint32_t* src, bool ro, const
                            if (x[k] >= top) ++above;
                            else if (x[k] >= L) atomicAdd(&bins[(top - 1 - x[k]) / w], 1u);
                          }
-                       }, KC_CUT_EVAL && (KC_CUT_LISTS || ro) ? dc.at(L) : 0xffffffffu, KC_CUT_EVAL && ro && dc.t);
+                       }, KC_CUT_EVAL && (KC_CUT_LISTS || ro) ? dc.at(L) : 0xffffffffu, KC_CUT_EVAL && ro && dc.sorted);
     __syncwarp();
     const uint32_t C = __reduce_add_sync(FULL, above);
     if (top == cap && C >= cap) return make_uint2(cap, C);  // no drop (round 0 only)
@@ -459,7 +460,7 @@ __device__ __noinline__ void cta_window(const uint32_t* src, bool ro, const EstT
                                       if (x[k] >= top) ++above;
                                       else if (x[k] >= L) atomicAdd(&s_hist[(top - 1 - x[k]) / w], 1u);
                                     }
-                                  }, KC_CUT_EVAL && (KC_CUT_LISTS || ro) ? dc.at(L) : 0xffffffffu, KC_CUT_EVAL && ro && dc.t);
+                                  }, KC_CUT_EVAL && (KC_CUT_LISTS || ro) ? dc.at(L) : 0xffffffffu, KC_CUT_EVAL && ro && dc.sorted);
     const uint32_t C = block_sum(above, s_red);
     if (top == cap && C >= cap) {  // no drop (round 0 only)
       if (tid == 0) {
@@ -667,7 +668,7 @@ __device__ __forceinline__ void eval_warp(const CP<OffT, EstT>& p, const View<Es
     if (lane_id() == 0) finish_eval(p, it, it.spec_t, it.spec_c, 0u, acc);
     return;
   }
-  if (KC_R0_SORTED && v.r0 && p.dc.t) {
+  if (KC_R0_SORTED && v.r0 && p.dc.sorted) {
     uint32_t scanned = 0;
     const uint2 tc = r0_sorted_warp(p, it.ob, it.deg, it.cap, scanned);
     if (lane_id() == 0) finish_eval(p, it, tc.x, tc.y, scanned, acc);
@@ -1024,7 +1025,7 @@ __device__ __forceinline__ void eval_sub_impl(const CP<OffT, EstT>& p, const Vie
   const EstT* snap = v.snap;
   const uint32_t cache_n = v.cache_n;
   const bool r0 = v.r0;
-  const bool r0s = KC_R0_SORTED && r0 && p.dc.t;
+  const bool r0s = KC_R0_SORTED && r0 && p.dc.sorted;
   for_class(p, v, C_SUB, GMAX_SMALL, [&](uint32_t mu, uint32_t n) {
     // metadata of the grab, one lane per item, loaded in parallel
     uint64_t mob = 0;
@@ -1161,7 +1162,7 @@ __device__ __forceinline__ void eval_thread_impl(const CP<OffT, EstT>& p, const 
   constexpr int R = DEG_THREAD_MAX;
   const EstT* snap = v.snap;
   const uint32_t cache_n = v.cache_n;
-  const bool r0s = KC_R0_SORTED && v.r0 && p.dc.t;
+  const bool r0s = KC_R0_SORTED && v.r0 && p.dc.sorted;
   for_class_lanes<TU>(p, v, C_THREAD, GMAX_THREAD, [&](const uint32_t(&u)[TU], uint32_t valid) {
     uint64_t ob[TU];
     uint32_t deg[TU], cap[TU], x[TU][R];
@@ -1292,7 +1293,7 @@ __device__ __forceinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const E
                            if (keep >> k & 1) p.radj[ob + pos++] = ids[k];
                          cursor += __shfl_sync(FULL, incl, 31);
                        }
-                     }, KC_CUT_NOTIFY && (KC_CUT_LISTS || ro) ? p.dc.at(need) : 0xffffffffu, KC_CUT_NOTIFY && ro && p.dc.t);
+                     }, KC_CUT_NOTIFY && (KC_CUT_LISTS || ro) ? p.dc.at(need) : 0xffffffffu, KC_CUT_NOTIFY && ro && p.dc.sorted);
   if (tag) {
     __syncwarp();
     const uint32_t C = __reduce_add_sync(FULL, above);
@@ -1365,7 +1366,7 @@ __device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p, const Enq& 
                                     for (int k = 0; k < 8; ++k)
                                       if (keep >> k & 1) p.radj[ob + pos++] = ids[k];
                                   }
-                                }, KC_CUT_NOTIFY && (KC_CUT_LISTS || ro) ? p.dc.at(need) : 0xffffffffu, KC_CUT_NOTIFY && ro && p.dc.t);
+                                }, KC_CUT_NOTIFY && (KC_CUT_LISTS || ro) ? p.dc.at(need) : 0xffffffffu, KC_CUT_NOTIFY && ro && p.dc.sorted);
   if (tag) {  // CTA suffix scan of the spec window (one pass, no refinement)
     const uint32_t C = block_sum(above, sh.red);
     constexpr int PER = (HIST_BINS + SOLVE_THREADS - 1) / SOLVE_THREADS;
@@ -1867,7 +1868,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     huge_warps(p, v, sh, ctl, 0, [&](uint32_t u) {
       const Item it = eval_item(p, v, s_cache, u);  // metadata loaded once
       // (round 0 on sorted rows reads a prefix only: always a warp's)
-      if (it.len > WARP_MAX_LEN && !(KC_R0_SORTED && v.r0 && p.dc.t)) return false;
+      if (it.len > WARP_MAX_LEN && !(KC_R0_SORTED && v.r0 && p.dc.sorted)) return false;
       eval_warp(p, v, s_cache, w_bins, it, acc);
       return true;
     });
@@ -1990,6 +1991,7 @@ CP<OffT, EstT> make_params(const SolveBuffers& b) {
   p.adj = b.adj;
   p.dc.t = KC_DCUT ? b.dcut : nullptr;
   p.dc.n = b.dcut_n;
+  p.dc.sorted = p.dc.t && b.rows_sorted;
   p.radj = b.radj;
   p.rlen = b.rlen;
   p.rthr = static_cast<EstT*>(b.rthr);

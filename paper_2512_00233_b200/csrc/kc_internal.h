@@ -56,8 +56,9 @@ struct SolveBuffers {
   // layout (owned by kc_graph)
   const void* off;           // uint32 or uint64, n_nz + 1 (relabelled ids)
   const uint32_t* adj;       // relabelled neighbours (+ ADJ_PAD)
-  const uint32_t* dcut;      // rows sorted: degree cut table [dcut_n] (kc_count.cu DegCut)
+  const uint32_t* dcut;      // degree cut table [dcut_n] (kc_count.cu DegCut)
   uint32_t dcut_n;
+  bool rows_sorted;          // neighbour rows sorted ascending
   uint32_t n_nz;
   uint32_t cls_begin[NCLS + 1];
   // est[0] = E, the round's snapshot; est[1] = N, the settled values (N == E
@@ -156,7 +157,8 @@ struct PrepOut {
   void* off;        // OffT [n_nz + 1]
   uint32_t* adj;    // [nnz]
   uint32_t* perm;   // [n] new id -> caller id
-  uint32_t* dcut;   // rows sorted only: dcut[x] = #{ids of degree >= x}, x <= max_degree + 1
+  uint32_t* dcut;   // dcut[x] = #{ids of degree >= x}, x <= max_degree + 1
+  bool rows_sorted; // rows sorted ascending (dcut then also splits every row)
   uint32_t n_nz;    // non-isolated vertices (ids [0, n_nz))
   uint32_t h_graph; // h-index of the degree sequence
   uint32_t max_degree;

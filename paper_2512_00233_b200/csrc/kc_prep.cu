@@ -32,18 +32,22 @@ __global__ void degrees_kernel(const uint64_t* __restrict__ off, uint32_t n,
   }
 }
 
-// dcut[x] = #{new ids of degree >= x} from the degrees sorted descending:
-// id w sets the x in (deg(w + 1), deg(w)]; dcut[0] = all, dcut[max + 1] = 0.
+// dcut[x] = #{new ids of degree >= x} from the degrees sorted descending
+// (binary search per x, all x in parallel); dcut[0] = all, dcut[max + 1] = 0.
 __global__ void degcut_kernel(const uint32_t* __restrict__ sdeg, uint32_t n_nz, uint32_t max_deg,
                               uint32_t* __restrict__ dcut) {
   const uint32_t gs = gridDim.x * blockDim.x;
-  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_nz; w += gs) {
-    const uint32_t d = sdeg[w], dn = w + 1 < n_nz ? sdeg[w + 1] : 0u;
-    for (uint32_t x = dn + 1; x <= d; ++x) dcut[x] = w + 1;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    dcut[0] = 0xffffffffu;
-    dcut[max_deg + 1] = 0;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= max_deg + 1; x += gs) {
+    if (x == 0) {
+      dcut[0] = 0xffffffffu;
+      continue;
+    }
+    uint32_t lo = 0, hi = n_nz;  // first w with sdeg[w] < x
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (sdeg[mid] >= x) lo = mid + 1; else hi = mid;
+    }
+    dcut[x] = lo;
   }
 }
 
@@ -197,6 +201,7 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
   out->adj = nullptr;
   out->perm = nullptr;
   out->dcut = nullptr;
+  out->rows_sorted = false;
   uint32_t* dcut = nullptr;
 
   PREP_CK(dalloc(&deg, n, s));
@@ -340,11 +345,12 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
                                                      (int64_t)n_nz, o, o + 1, s));
         }
         std::swap(new_adj, sort_tmp);
-        // rows are sorted: the degree cut table (kc_count.cu DegCut)
-        PREP_CK(dalloc(&dcut, (size_t)out->max_degree + 2, s));
-        degcut_kernel<<<G, B, 0, s>>>(sdeg, n_nz, out->max_degree, dcut);
-        PREP_CK(cudaGetLastError());
+        out->rows_sorted = true;
       }
+      // the degree cut table (kc_count.cu DegCut)
+      PREP_CK(dalloc(&dcut, (size_t)out->max_degree + 2, s));
+      degcut_kernel<<<G, B, 0, s>>>(sdeg, n_nz, out->max_degree, dcut);
+      PREP_CK(cudaGetLastError());
     }
     PREP_CK(cudaStreamSynchronize(s));
   }
