@@ -127,11 +127,11 @@ constexpr int WQ = KC_WQ;          // per-warp, per-class enqueue buffer (flushe
 #define KC_LIST_SHIFT 1            // list threshold L = t - (t >> KC_LIST_SHIFT)
 #endif
 
-// Degree cut table (degree-sorted layouts only).  New ids are assigned in
-// order of non-increasing degree, so cut(x) = #{ids of degree >= x} splits
-// every row: id < cut(x) iff degree >= x.  Estimates never exceed degrees,
-// hence id >= cut(x) implies estimate < x — those entries can be skipped
-// without a gather, and in a row sorted ascending they form its suffix.
+// Degree cut table.  New ids are assigned in order of non-increasing degree,
+// so cut(x) = #{ids of degree >= x} splits the ids: id < cut(x) iff degree
+// >= x.  Estimates never exceed degrees, hence id >= cut(x) implies estimate
+// < x — those entries can be skipped without a gather, and in a row sorted
+// ascending (sorted layouts) they form its suffix.
 struct DegCut {
   const uint32_t* t;  // [n]; nullptr: no table
   uint32_t n;         // max degree + 2
