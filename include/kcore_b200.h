@@ -131,8 +131,9 @@ kc_status kc_graph_upload_device(const kc_csr_view* csr, int device, kc_graph** 
 #define KC_UPLOAD_FORCE_OFF64 1u /* 64-bit device offsets even when nnz < 2^32 */
 #define KC_UPLOAD_FORCE_EST32 2u /* 32-bit estimates even when H < 2^15 */
 #define KC_UPLOAD_UNSORTED_ROWS 4u /* keep relabelled rows in input order: skips the
-                                      per-row sort (~10 ms on R-MAT 22) at 5-20% slower
-                                      solves — for one-shot solves (kc_fastk_run) */
+                                      per-row sort (~10 ms on R-MAT 22) at 13-75% slower
+                                      solves (no sorted-row degree cuts) — for one-shot
+                                      solves (kc_fastk_run) */
 kc_status kc_graph_upload_ex(const kc_csr_view* csr, int device, int on_device, uint32_t flags,
                              kc_graph** out);
 void kc_graph_free(kc_graph* g);
