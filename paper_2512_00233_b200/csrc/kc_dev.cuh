@@ -290,10 +290,12 @@ __device__ __forceinline__ uint32_t tile8_sum(uint32_t v) {
 // to the callback.  Rows need not be 16-byte aligned: positions outside
 // [ob, oe) are masked (id arrays have ADJ_PAD spare entries).
 // ------------------------------------------------------------------------
+// `cut` / `stop`: as in stream_row_rt below.
 template <int NT, bool RO, typename EstT, typename F>
 __device__ __forceinline__ void stream_row(const uint32_t* src, const EstT* snap, uint32_t me,
                                            uint64_t ob, uint64_t oe, const EstT* s_cache,
-                                           uint32_t cache_n, F&& f) {
+                                           uint32_t cache_n, F&& f, uint32_t cut = 0xffffffffu,
+                                           bool stop = false) {
   constexpr uint64_t STEP = (uint64_t)NT * 8;
   uint64_t a = ob & ~(uint64_t)3;
   uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
@@ -306,15 +308,19 @@ __device__ __forceinline__ void stream_row(const uint32_t* src, const EstT* snap
     if (nb + 4 * me + 4 * NT < oe) n1 = ld_ids4<RO>(src, nb + 4 * me + 4 * NT);
     uint32_t ids[8], x[8];
     uint32_t ok = 0;
+    bool past = false;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const uint64_t pos = a + 4 * me + (k >> 2) * 4 * NT + (k & 3);
       ids[k] = u4_get(k < 4 ? q0 : q1, k & 3);
-      const bool v = pos >= ob && pos < oe;
+      const bool in = pos >= ob && pos < oe;
+      const bool v = in && ids[k] < cut;
+      past |= in && !v;
       ok |= (uint32_t)v << k;
       x[k] = v ? est_at(s_cache, cache_n, snap, ids[k]) : 0u;
     }
     f(ok, ids, x);
+    if (stop && __any_sync(FULL, past)) break;
     q0 = n0;
     q1 = n1;
   }

@@ -41,6 +41,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef KC_SOLVE_DCUT
+#define KC_SOLVE_DCUT 1  // degree cut table in the reference-rule scans
+#endif
+
 namespace kcb {
 namespace {
 using namespace dev;
@@ -71,7 +75,22 @@ struct P {
   uint32_t cache_n;
   uint32_t clamp_drop;  // max degree > H: the reference's round 0 lowers deg -> <= H
   uint32_t tail_batch;  // hybrid_tail: switch threshold (0 = off)
+  const uint32_t* dcut;  // degree cut table (kc_count.cu DegCut), dcut_n entries
+  uint32_t dcut_n;
+  bool sorted;           // rows sorted ascending: scans stop at the first id >= their cut
 };
+
+// Ids >= id_cut(x) have degree, hence estimate, < x: skipped without a gather.
+template <typename OffT, typename EstT>
+__device__ __forceinline__ uint32_t id_cut(const P<OffT, EstT>& p, uint32_t x) {
+  return !p.dcut ? 0xffffffffu : x < p.dcut_n ? p.dcut[x] : 0u;
+}
+
+__device__ __forceinline__ uint32_t window_floor(uint32_t top, uint32_t bins, uint32_t lo) {
+  uint32_t f = top > bins ? top - bins : 0u;
+  if (lo > f) f = lo;
+  return f ? f : 1u;
+}
 
 // Per-round view: what this round reads and writes.
 template <typename EstT>
@@ -240,7 +259,7 @@ __device__ __noinline__ void huge_window(const P<OffT, EstT>& p, const RoundView
 #pragma unroll
                                 for (int k = 0; k < 8; ++k)
                                   if (ok >> k & 1) tally<HIST_BINS>(x[k], top, lo, above, s_hist);
-                              });
+                              }, id_cut(p, window_floor(top, HIST_BINS, lo)), p.sorted);
     const uint32_t C = block_sum(above, s_red);
     constexpr int PER = (HIST_BINS + SOLVE_THREADS - 1) / SOLVE_THREADS;  // bins per thread
     uint32_t h[PER];
@@ -301,7 +320,7 @@ __device__ void eval_huge(const P<OffT, EstT>& p, const RoundView<EstT>& rv, con
                                 [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
                                   for (int k = 0; k < 8; ++k) c += (ok >> k & 1) && x[k] >= cap;
-                                });
+                                }, id_cut(p, cap), p.sorted);
       cA = block_sum(c, s_red);
       keep = cA >= cap;
     }
@@ -367,7 +386,7 @@ __device__ __noinline__ uint2 warp_window(const P<OffT, EstT>& p, const RoundVie
 #pragma unroll
                      for (int k = 0; k < 8; ++k)
                        if (ok >> k & 1) tally<WARP_BINS>(x[k], top, lo, above, bins);
-                   });
+                   }, id_cut(p, window_floor(top, WARP_BINS, lo)), p.sorted);
     __syncwarp();
     const uint32_t C = __reduce_add_sync(FULL, above);
     uint32_t level = 0, c = 0;
@@ -399,7 +418,7 @@ __device__ void eval_wstream(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
                        [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
                          for (int k = 0; k < 8; ++k) c += (ok >> k & 1) && x[k] >= cap;
-                       });
+                       }, id_cut(p, cap), p.sorted);
         cA = __reduce_add_sync(FULL, c);
         keep = cA >= cap;
       }
@@ -516,10 +535,11 @@ __device__ void notify_huge(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
     if (t < cap) {
       const uint64_t ob = p.off[u], oe = p.off[u + 1];
       if (tid == 0) acc.nscan += oe - ob;
+      // only N[w] > t notifies (both guards): ids >= cut(t + 1) cannot
       stream_row<SOLVE_THREADS, true>(p.adj, p.N, tid, ob, oe, s_cache, rv.cache_n,
                                 [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
                                   notify_batch<8>(p, rv, ok, ids, x, t, cap, acc);
-                                });
+                                }, id_cut(p, t + 1), p.sorted);
       if (tid == 0) p.E[u] = (EstT)t;  // apply (fastk.cpp:153)
     }
     __syncthreads();
@@ -542,7 +562,7 @@ __device__ void notify_wstream(const P<OffT, EstT>& p, const RoundView<EstT>& rv
       stream_row<32, true>(p.adj, (const EstT*)p.N, lane, it.ob, it.oe, s_cache, rv.cache_n,
                      [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
                        notify_batch<8>(p, rv, ok, ids, x, t, it.cap, acc);
-                     });
+                     }, id_cut(p, t + 1), p.sorted);
       if (lane == 0) p.E[it.u] = (EstT)t;
     }
   });
@@ -767,6 +787,9 @@ P<OffT, EstT> make_params(const SolveBuffers& b) {
   P<OffT, EstT> p{};
   p.off = static_cast<const OffT*>(b.off);
   p.adj = b.adj;
+  p.dcut = KC_SOLVE_DCUT ? b.dcut : nullptr;
+  p.dcut_n = b.dcut_n;
+  p.sorted = p.dcut && b.rows_sorted;
   p.n_nz = b.n_nz;
   for (int c = 0; c <= NCLS; ++c) p.cb[c] = b.cls_begin[c];
   p.E = static_cast<EstT*>(b.est[0]);
