@@ -610,56 +610,6 @@ __device__ __forceinline__ void finish_eval(const CP<OffT, EstT>& p, const Item&
   if (it.thr != 0 && t < it.thr) p.rthr[it.u] = 0;
 }
 
-// Round 0 on a degree-sorted row (p.dc.t set): the snapshot is E = min(deg,
-// H), non-increasing along the row, so d_i >= i (1-based positions) holds
-// exactly on a prefix and the capped h-index is t = #{i <= cap : row[i-1] <
-// cut(i)}; count(E >= t) = #{j : row[j] < cut(t)}, a prefix of length >= t.
-// Both read the row and the contiguous cut table only — no gathers — and
-// stop at the first position that fails.  Returns (t, count(>= t)).
-template <typename OffT, typename EstT>
-__device__ __forceinline__ uint2 r0_sorted_warp(const CP<OffT, EstT>& p, uint64_t ob, uint32_t deg,
-                                                uint32_t cap, uint32_t& scanned) {
-  const uint32_t lane = lane_id();
-  const uint32_t m = cap < deg ? cap : deg;
-  uint32_t h = 0, i0 = 0;
-  for (; i0 < m; i0 += 256) {
-    uint32_t id[8], ct[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t i = i0 + 32 * k + lane;  // 0-based position
-      id[k] = i < m ? __ldg(p.adj + ob + i) : 0xffffffffu;
-      ct[k] = i < m ? __ldg(p.dc.t + i + 1) : 0u;
-    }
-    bool miss = false;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const bool in = i0 + 32 * k + lane < m;
-      h += in && id[k] < ct[k];
-      miss |= in && !(id[k] < ct[k]);
-    }
-    if (__any_sync(FULL, miss)) break;
-  }
-  const uint32_t t = __reduce_add_sync(FULL, h);
-  const uint32_t ctt = __ldg(p.dc.t + t);
-  uint32_t c = 0, j0 = t;
-  for (; j0 < deg; j0 += 256) {
-    uint32_t id[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t j = j0 + 32 * k + lane;
-      id[k] = j < deg ? __ldg(p.adj + ob + j) : 0xffffffffu;
-    }
-    bool miss = false;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      c += id[k] < ctt;
-      miss |= j0 + 32 * k + lane < deg && !(id[k] < ctt);
-    }
-    if (__any_sync(FULL, miss)) break;
-  }
-  scanned = (i0 < m ? i0 + 256 : m) + (j0 < deg ? j0 + 256 - t : deg - t);
-  return make_uint2(t, t + __reduce_add_sync(FULL, c));
-}
 
 template <typename OffT, typename EstT, typename A>
 __device__ __forceinline__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
@@ -670,7 +620,7 @@ __device__ __forceinline__ void eval_warp(const CP<OffT, EstT>& p, const View<Es
   }
   if (KC_R0_SORTED && v.r0 && p.dc.sorted) {
     uint32_t scanned = 0;
-    const uint2 tc = r0_sorted_warp(p, it.ob, it.deg, it.cap, scanned);
+    const uint2 tc = r0_sorted_warp(p.adj, p.dc.t, it.ob, it.deg, it.cap, scanned);
     if (lane_id() == 0) finish_eval(p, it, tc.x, tc.y, scanned, acc);
     return;
   }

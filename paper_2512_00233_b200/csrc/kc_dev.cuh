@@ -373,6 +373,57 @@ __device__ __forceinline__ void stream_row_rt(const uint32_t* src, bool ro, cons
   }
 }
 
+// Round 0 on a degree-sorted row (`dcut`: the degree cut table, kc_count.cu
+// DegCut): the snapshot is E = min(deg, H), non-increasing along the row, so d_i >= i (1-based positions) holds
+// exactly on a prefix and the capped h-index is t = #{i <= cap : row[i-1] <
+// cut(i)}; count(E >= t) = #{j : row[j] < cut(t)}, a prefix of length >= t.
+// Both read the row and the contiguous cut table only — no gathers — and
+// stop at the first position that fails.  Returns (t, count(>= t)).
+__device__ __forceinline__ uint2 r0_sorted_warp(const uint32_t* adj, const uint32_t* dcut,
+                                                uint64_t ob, uint32_t deg, uint32_t cap,
+                                                uint32_t& scanned) {
+  const uint32_t lane = lane_id();
+  const uint32_t m = cap < deg ? cap : deg;
+  uint32_t h = 0, i0 = 0;
+  for (; i0 < m; i0 += 256) {
+    uint32_t id[8], ct[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t i = i0 + 32 * k + lane;  // 0-based position
+      id[k] = i < m ? __ldg(adj + ob + i) : 0xffffffffu;
+      ct[k] = i < m ? __ldg(dcut + i + 1) : 0u;
+    }
+    bool miss = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool in = i0 + 32 * k + lane < m;
+      h += in && id[k] < ct[k];
+      miss |= in && !(id[k] < ct[k]);
+    }
+    if (__any_sync(FULL, miss)) break;
+  }
+  const uint32_t t = __reduce_add_sync(FULL, h);
+  const uint32_t ctt = __ldg(dcut + t);
+  uint32_t c = 0, j0 = t;
+  for (; j0 < deg; j0 += 256) {
+    uint32_t id[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t j = j0 + 32 * k + lane;
+      id[k] = j < deg ? __ldg(adj + ob + j) : 0xffffffffu;
+    }
+    bool miss = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      c += id[k] < ctt;
+      miss |= j0 + 32 * k + lane < deg && !(id[k] < ctt);
+    }
+    if (__any_sync(FULL, miss)) break;
+  }
+  scanned = (i0 < m ? i0 + 256 : m) + (j0 < deg ? j0 + 256 - t : deg - t);
+  return make_uint2(t, t + __reduce_add_sync(FULL, c));
+}
+
 template <typename EstT>
 __device__ __forceinline__ void fill_cache(EstT* s_cache, const EstT* src, uint32_t cache_n) {
   // cache_n * sizeof(EstT) is a multiple of 16 bytes; 8 loads in flight per

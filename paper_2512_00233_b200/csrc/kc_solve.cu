@@ -44,6 +44,9 @@ namespace cg = cooperative_groups;
 #ifndef KC_SOLVE_DCUT
 #define KC_SOLVE_DCUT 1  // degree cut table in the reference-rule scans
 #endif
+#ifndef KC_SOLVE_R0
+#define KC_SOLVE_R0 1    // round 0 on sorted rows by the prefix rule (r0_sorted_warp)
+#endif
 
 namespace kcb {
 namespace {
@@ -102,6 +105,7 @@ struct RoundView {
   bool count;        // counting rule
   bool ext;          // extended_notify (reference rule)
   bool skip_a;       // counting rule, r > 0: every active vertex drops
+  bool r0;           // round 0 (E = min(deg, H))
   uint32_t cache_n;  // ids cached in shared memory this round (0: none)
 };
 
@@ -312,6 +316,15 @@ __device__ void eval_huge(const P<OffT, EstT>& p, const RoundView<EstT>& rv, con
     if (u == 0xffffffffu) break;
     const uint64_t ob = p.off[u], oe = p.off[u + 1];
     const uint32_t cap = est_at(s_cache, rv.cache_n, rv.snap, u);
+    if (KC_SOLVE_R0 && rv.r0 && p.sorted) {  // a prefix of the row: one warp's
+      if (warp_id() == 0) {
+        uint32_t sc = 0;
+        const uint2 tc = r0_sorted_warp(p.adj, p.dcut, ob, (uint32_t)(oe - ob), cap, sc);
+        if (tid == 0) finish_eval(p, rv, u, tc.x, cap, tc.y, oe - ob, acc);
+      }
+      __syncthreads();
+      continue;
+    }
     bool keep = false;
     uint32_t cA = 0;
     if (!rv.skip_a) {
@@ -410,6 +423,12 @@ __device__ void eval_wstream(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
     for (uint32_t i = 0; i < n; ++i) {
       const Meta it = shfl_meta(mine, i);
       const uint32_t cap = it.cap;
+      if (KC_SOLVE_R0 && rv.r0 && p.sorted) {
+        uint32_t sc = 0;
+        const uint2 tc = r0_sorted_warp(p.adj, p.dcut, it.ob, (uint32_t)(it.oe - it.ob), cap, sc);
+        if (lane == 0) finish_eval(p, rv, it.u, tc.x, cap, tc.y, it.oe - it.ob, acc);
+        continue;
+      }
       bool keep = false;
       uint32_t cA = 0;
       if (!rv.skip_a) {
@@ -649,6 +668,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, KC_CTAS_PER_SM) rounds_kernel(P
     rv.count = count;
     rv.ext = p.rule != R_REF_PLAIN;
     rv.skip_a = count && r > 0;
+    rv.r0 = r == 0;
     unsigned long long* pf = (p.prof && r < PROF_ROUNDS && tid == 0)
                                  ? p.prof + ((size_t)r * gridDim.x + blockIdx.x) * PROF_PHASES
                                  : nullptr;
