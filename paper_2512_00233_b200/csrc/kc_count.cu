@@ -67,6 +67,8 @@ using namespace dev;
 #define KC_GMAX_SMALL 32
 #endif
 constexpr uint32_t GMAX_BIG = KC_GMAX_BIG, GMAX_WARP = KC_GMAX_WARP, GMAX_SMALL = KC_GMAX_SMALL;  // items per grab (max)
+static_assert(GMAX_BIG <= 32 && GMAX_WARP <= 32 && GMAX_SMALL <= 32,
+              "a grab's items are held one per lane");
 constexpr uint32_t CACHE_MIN_ACTIVE = KC_CACHE_MIN_ACTIVE;  // smaller rounds skip the shared-memory cache
 #ifndef KC_LIST_MIN_DEG
 #define KC_LIST_MIN_DEG 64
