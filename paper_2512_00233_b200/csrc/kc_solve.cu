@@ -476,6 +476,20 @@ __device__ void eval_sub(const P<OffT, EstT>& p, const RoundView<EstT>& rv, cons
           const uint32_t q = k + 8 * j;
           ids[j] = q < deg ? p.adj[it.ob + q] : 0xffffffffu;
         }
+        if (KC_SOLVE_R0 && rv.r0 && p.sorted) {  // prefix rule on the ids (r0_sorted_warp)
+          const uint32_t m = deg < cap ? deg : cap;
+          uint32_t hc = 0;
+#pragma unroll
+          for (int j = 0; j < R; ++j) hc += k + 8 * j < m && ids[j] < __ldg(p.dcut + k + 8 * j + 1);
+          const uint32_t t = tile8_sum(hc);
+          const uint32_t ct = __ldg(p.dcut + t);
+          uint32_t cc = 0;
+#pragma unroll
+          for (int j = 0; j < R; ++j) cc += ids[j] < ct;
+          const uint32_t c = tile8_sum(cc);
+          if (has && k == 0) finish_eval(p, rv, it.u, t, cap, t ? c : deg, deg, acc);
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < R; ++j)
           if (ids[j] != 0xffffffffu) vals.set(j, est_at(s_cache, rv.cache_n, rv.snap, ids[j]));
@@ -516,10 +530,22 @@ __device__ void eval_thread(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
     const uint32_t cap = est_at(s_cache, rv.cache_n, rv.snap, u);
     uint32_t x[R];
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const uint32_t id = (uint32_t)j < deg ? p.adj[ob + j] : 0xffffffffu;
-      x[j] = id != 0xffffffffu ? est_at(s_cache, rv.cache_n, rv.snap, id) : 0u;
+    for (int j = 0; j < R; ++j) x[j] = (uint32_t)j < deg ? p.adj[ob + j] : 0xffffffffu;
+    if (KC_SOLVE_R0 && rv.r0 && p.sorted) {  // prefix rule on the ids (r0_sorted_warp)
+      const uint32_t m = deg < cap ? deg : cap;
+      uint32_t t = 0;
+#pragma unroll
+      for (int j = 0; j < R; ++j) t += (uint32_t)j < m && x[j] < __ldg(p.dcut + j + 1);
+      const uint32_t ct = __ldg(p.dcut + t);
+      uint32_t c = 0;
+#pragma unroll
+      for (int j = 0; j < R; ++j) c += x[j] < ct;
+      finish_eval(p, rv, u, t, cap, t ? c : deg, deg, acc);
+      return;
     }
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      x[j] = x[j] != 0xffffffffu ? est_at(s_cache, rv.cache_n, rv.snap, x[j]) : 0u;
     uint32_t h = 0;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
