@@ -117,7 +117,8 @@ constexpr int WQ = KC_WQ;          // per-warp, per-class enqueue buffer (flushe
 #define KC_CUT_EVAL 1              // windowed evaluations skip / stop at ids below their floor
 #endif
 #ifndef KC_CUT_NOTIFY
-#define KC_CUT_NOTIFY 0            // notify scans likewise (measured slower: rows 0-1 gain little)
+#define KC_CUT_NOTIFY 0            // notify row scans likewise, in their own function (R-MAT 26 -2.5%,
+                                   // R-MAT 22 +0.6%, Chung-Lu +1.1%: off)
 #endif
 #ifndef KC_CUT_LISTS
 #define KC_CUT_LISTS 1             // ... also on (unsorted) lists: mask only
@@ -1206,7 +1207,7 @@ __device__ __forceinline__ uint32_t list_threshold(uint32_t t) {
 
 // Returns the notifications fired by this lane (counted once per warp in
 // `acc` by the callers).
-template <typename OffT, typename EstT>
+template <bool CUT, typename OffT, typename EstT>
 __device__ __forceinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const Enq& q,
                                              const EstT* s_cache, uint32_t cache_n,
                                              uint32_t* bins, const uint32_t* src, bool ro, uint32_t u,
@@ -1245,7 +1246,7 @@ __device__ __forceinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const E
                            if (keep >> k & 1) p.radj[ob + pos++] = ids[k];
                          cursor += __shfl_sync(FULL, incl, 31);
                        }
-                     }, KC_CUT_NOTIFY && (KC_CUT_LISTS || ro) ? p.dc.at(need) : 0xffffffffu, KC_CUT_NOTIFY && ro && p.dc.sorted);
+                     }, CUT ? p.dc.at(need) : 0xffffffffu, CUT && ro && p.dc.sorted);
   if (tag) {
     __syncwarp();
     const uint32_t C = __reduce_add_sync(FULL, above);
@@ -1373,6 +1374,16 @@ struct Drop {
 };
 
 template <typename OffT, typename EstT>
+__device__ __noinline__ uint32_t notify_row_warp(const CP<OffT, EstT>& p, const Enq& q,
+                                                 const EstT* s_cache, uint32_t cache_n,
+                                                 uint32_t* bins, uint32_t u, uint64_t ob,
+                                                 uint32_t len, uint32_t t, uint32_t cap,
+                                                 uint32_t build, uint32_t tag) {
+  return notify_warp<true>(p, q, s_cache, cache_n, bins, p.adj, true, u, ob, len, t, cap, build,
+                           tag, 1u);
+}
+
+template <typename OffT, typename EstT>
 __device__ __forceinline__ Drop drop_item(const CP<OffT, EstT>& p, uint32_t u) {
   Drop d;
   d.u = u;
@@ -1409,10 +1420,13 @@ __device__ __forceinline__ uint32_t notify_drop_warp(const CP<OffT, EstT>& p, co
   const uint32_t tag = KC_SPEC ? round + 1 : 0u;
   // a list (optionally filtered in place), or the CSR row (building the list)
   const bool lst = d.thr != 0;
-  return notify_warp(p, q, s_cache, cache_n, bins, lst ? (const uint32_t*)p.radj : p.adj, !lst,
-                     d.u, d.ob, d.len, d.t, d.cap,
-                     lst ? (KC_LIST_COMPACT ? d.thr : 0u) : list_build(round == 0, d), tag,
-                     lst ? d.thr : 1u);
+  if (KC_CUT_NOTIFY && !lst)  // CSR row: its own code (and register budget), cut at `need`
+    return notify_row_warp(p, q, s_cache, cache_n, bins, d.u, d.ob, d.len, d.t, d.cap,
+                           list_build(round == 0, d), tag);
+  return notify_warp<false>(p, q, s_cache, cache_n, bins, lst ? (const uint32_t*)p.radj : p.adj,
+                            !lst, d.u, d.ob, d.len, d.t, d.cap,
+                            lst ? (KC_LIST_COMPACT ? d.thr : 0u) : list_build(round == 0, d), tag,
+                            lst ? d.thr : 1u);
 }
 
 template <typename OffT, typename EstT, typename A>
