@@ -44,6 +44,10 @@ namespace cg = cooperative_groups;
 #ifndef KC_SOLVE_DCUT
 #define KC_SOLVE_DCUT 1  // degree cut table in the reference-rule scans
 #endif
+#ifndef KC_SOLVE_FINE
+#define KC_SOLVE_FINE 1  // hub windows: the 256 levels below cap first (sorted rows)
+#endif
+constexpr uint32_t HUB_FINE = 256;
 #ifndef KC_SOLVE_R0
 #define KC_SOLVE_R0 1    // round 0 on sorted rows by the prefix rule (r0_sorted_warp)
 #endif
@@ -254,7 +258,12 @@ __device__ __noinline__ void huge_window(const P<OffT, EstT>& p, const RoundView
                                          uint32_t* out) {
   const uint32_t tid = threadIdx.x;
   uint32_t top = cap;
+  // sorted rows: the FINE levels below cap first — most drops are small, and
+  // that window's cut reads a short prefix of a hub's row
+  bool fine = KC_SOLVE_FINE && p.sorted && cap > HUB_FINE;
   for (;;) {
+    const uint32_t fl = fine && top - HUB_FINE > lo ? top - HUB_FINE : lo;  // tally floor
+    const int minx = fine ? (int)(top - HUB_FINE) : 1;  // levels this pass decides
     for (int i = tid; i < HIST_BINS; i += SOLVE_THREADS) s_hist[i] = 0;
     __syncthreads();
     uint32_t above = 0;
@@ -262,8 +271,9 @@ __device__ __noinline__ void huge_window(const P<OffT, EstT>& p, const RoundView
                               [&](uint32_t ok, const uint32_t(&)[8], const uint32_t(&x)[8]) {
 #pragma unroll
                                 for (int k = 0; k < 8; ++k)
-                                  if (ok >> k & 1) tally<HIST_BINS>(x[k], top, lo, above, s_hist);
-                              }, id_cut(p, window_floor(top, HIST_BINS, lo)), p.sorted);
+                                  if (ok >> k & 1) tally<HIST_BINS>(x[k], top, fl, above, s_hist);
+                              }, id_cut(p, window_floor(top, fine ? HUB_FINE : HIST_BINS, lo)),
+                              p.sorted);
     const uint32_t C = block_sum(above, s_red);
     constexpr int PER = (HIST_BINS + SOLVE_THREADS - 1) / SOLVE_THREADS;  // bins per thread
     uint32_t h[PER];
@@ -280,7 +290,7 @@ __device__ __noinline__ void huge_window(const P<OffT, EstT>& p, const RoundView
       run += h[j];
       const int i = tid * PER + j;
       const int x = i < HIST_BINS ? (int)top - 1 - i : 0;  // x = 0 never qualifies
-      if (found == 0xffffffffu && x >= 1 && run >= (uint32_t)x) {
+      if (found == 0xffffffffu && x >= minx && run >= (uint32_t)x) {
         found = (uint32_t)i;
         frun = run;
       }
@@ -293,6 +303,12 @@ __device__ __noinline__ void huge_window(const P<OffT, EstT>& p, const RoundView
       }
       __syncthreads();
       return;
+    }
+    if (fine) {  // no level in [top - HUB_FINE, top) qualifies: the regular windows below
+      fine = false;
+      top -= HUB_FINE;
+      __syncthreads();
+      continue;
     }
     if ((int)top - HIST_BINS <= 0) {
       if (tid == 0) {
