@@ -35,6 +35,7 @@ namespace {
 constexpr int TB = 1024;                    // tail CTA
 constexpr int TW = TB / 32;
 constexpr uint32_t TAIL_BINS = 16384;       // h-index histogram (64 KB shared)
+constexpr uint32_t KEYCAP = 4096;           // active list mirrored in shared memory up to this size
 constexpr unsigned FULLM = 0xffffffffu;
 
 struct TailState {     // device scalars
@@ -209,6 +210,12 @@ template <typename OffT, typename EstT>
 __global__ void __launch_bounds__(TB, 1) tail_kernel(TP<OffT, EstT> p) {
   if (!tail_on(p)) return;
   extern __shared__ uint32_t hist[];
+  // The active list's pop keys (est, caller id) never change while an entry
+  // waits (only the popped vertex's estimate moves), so while the list holds
+  // at most KEYCAP entries it is mirrored in shared memory: the argmin of a
+  // pop reads no global memory.  Past KEYCAP the global list alone is used.
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(hist + TAIL_BINS);
+  uint32_t* s_id = reinterpret_cast<uint32_t*>(s_key + KEYCAP);
   __shared__ unsigned long long red64[33];
   __shared__ uint32_t red[33];
   __shared__ uint32_t s_m, s_idx, s_u, s_fires;
@@ -217,21 +224,30 @@ __global__ void __launch_bounds__(TB, 1) tail_kernel(TP<OffT, EstT> p) {
   if (tid == 0) s_m = p.ts->m;
   __syncthreads();
   const uint32_t m0 = s_m;
+  bool mir = m0 <= KEYCAP;
+  if (mir)
+    for (uint32_t i = tid; i < m0; i += TB) {
+      const uint32_t v = p.list[i];
+      s_id[i] = v;
+      s_key[i] = (unsigned long long)p.E[v] << 32 | p.perm[v];
+    }
+  __syncthreads();
   unsigned long long pops_done = 0, escan = 0, drops = 0, fires = 0;
   for (;;) {
     const uint32_t m = s_m;
     if (m == 0) break;
+    if (m > KEYCAP) mir = false;  // (uniform: s_m is read after a barrier)
     // the active vertex with the smallest (est, caller id)
     unsigned long long best = ~0ull;
     for (uint32_t i = tid; i < m; i += TB) {
-      const uint32_t v = p.list[i];
-      const unsigned long long key = (unsigned long long)p.E[v] << 32 | p.perm[v];
+      const unsigned long long key =
+          mir ? s_key[i] : (unsigned long long)p.E[p.list[i]] << 32 | p.perm[p.list[i]];
       best = key < best ? key : best;
     }
     const unsigned long long kmin = blk_min64(best, red64);
     for (uint32_t i = tid; i < m; i += TB) {
-      const uint32_t v = p.list[i];
-      if (((unsigned long long)p.E[v] << 32 | p.perm[v]) == kmin) {
+      const uint32_t v = mir ? s_id[i] : p.list[i];
+      if ((mir ? s_key[i] : (unsigned long long)p.E[v] << 32 | p.perm[v]) == kmin) {
         s_idx = i;  // keys are unique (perm is a bijection)
         s_u = v;
       }
@@ -239,6 +255,10 @@ __global__ void __launch_bounds__(TB, 1) tail_kernel(TP<OffT, EstT> p) {
     __syncthreads();
     const uint32_t u = s_u;
     if (tid == 0) {
+      if (mir) {
+        s_key[s_idx] = s_key[m - 1];
+        s_id[s_idx] = s_id[m - 1];
+      }
       p.list[s_idx] = p.list[m - 1];  // unordered list: swap-remove
       s_m = m - 1;
       act[u] = 0;  // fastk.cpp:41
@@ -267,7 +287,12 @@ __global__ void __launch_bounds__(TB, 1) tail_kernel(TP<OffT, EstT> p) {
         ++f;
         if (act[v] == 0) {  // a simple row holds v once: no race
           act[v] = 1;
-          p.list[atomicAdd(&s_m, 1u)] = v;
+          const uint32_t pos = atomicAdd(&s_m, 1u);
+          p.list[pos] = v;
+          if (pos < KEYCAP) {  // mirror (est does not change until v is popped)
+            s_id[pos] = v;
+            s_key[pos] = (unsigned long long)ev << 32 | p.perm[v];
+          }
         }
       }
       f = __reduce_add_sync(FULLM, f);
@@ -309,7 +334,7 @@ cudaError_t launch_tail_t(const SolveBuffers& b, const uint32_t* perm, int ext, 
   if (e != cudaSuccess) return e;
   tail_list_kernel<OffT, EstT><<<num_sms * 4, 256, 0, s>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const size_t smem = TAIL_BINS * sizeof(uint32_t);
+  const size_t smem = TAIL_BINS * sizeof(uint32_t) + KEYCAP * (sizeof(unsigned long long) + sizeof(uint32_t));
   e = cudaFuncSetAttribute(tail_kernel<OffT, EstT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
   if (e != cudaSuccess) return e;
