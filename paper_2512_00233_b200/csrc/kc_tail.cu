@@ -161,9 +161,10 @@ __device__ __forceinline__ uint32_t blk_suffix_excl(uint32_t v, uint32_t* red) {
 // compute_index_over (include/kcore/kernel.hpp:27-42) of u at cap, CTA-wide:
 // the largest t <= cap with #{neighbours: min(est, cap) >= t} >= t; 0 when
 // cap == 0.
+// e0: the estimate of entry tid (tid < deg), gathered by the caller.
 template <typename OffT, typename EstT>
 __device__ uint32_t tail_index(const TP<OffT, EstT>& p, uint64_t ob, uint32_t deg, uint32_t cap,
-                               uint32_t* hist, uint32_t* red) {
+                               uint32_t e0, uint32_t* hist, uint32_t* red) {
   if (cap == 0) return 0;  // kernel.hpp:30
   const uint32_t tid = threadIdx.x;
   if (cap < TAIL_BINS) {
@@ -171,7 +172,7 @@ __device__ uint32_t tail_index(const TP<OffT, EstT>& p, uint64_t ob, uint32_t de
     for (uint32_t i = tid; i <= cap; i += TB) hist[i] = 0;
     __syncthreads();
     for (uint32_t j = tid; j < deg; j += TB) {
-      const uint32_t e = p.E[p.adj[ob + j]];
+      const uint32_t e = j == tid ? e0 : p.E[p.adj[ob + j]];
       atomicAdd(&hist[e < cap ? e : cap], 1u);
     }
     __syncthreads();
@@ -269,7 +270,11 @@ __global__ void __launch_bounds__(TB, 1) tail_kernel(TP<OffT, EstT> p) {
     const uint32_t deg = (uint32_t)((uint64_t)p.off[u + 1] - ob);
     escan += deg;
     const uint32_t cap = p.E[u];
-    const uint32_t t = tail_index(p, ob, deg, cap, hist, red);  // fastk.cpp:43-44
+    // the first TB row entries and their estimates stay in registers for
+    // both scans of this pop (only u's own estimate changes in between)
+    const uint32_t v0 = tid < deg ? p.adj[ob + tid] : 0u;
+    const uint32_t e0 = tid < deg ? (uint32_t)p.E[v0] : 0u;
+    const uint32_t t = tail_index(p, ob, deg, cap, e0, hist, red);  // fastk.cpp:43-44
     if (t < cap) {  // fastk.cpp:45-46: apply immediately
       ++drops;
       __syncthreads();
@@ -280,8 +285,8 @@ __global__ void __launch_bounds__(TB, 1) tail_kernel(TP<OffT, EstT> p) {
       __syncthreads();
       uint32_t f = 0;
       for (uint32_t j = tid; j < deg; j += TB) {  // fastk.cpp:47-53
-        const uint32_t v = p.adj[ob + j];
-        const uint32_t ev = p.E[v];
+        const uint32_t v = j == tid ? v0 : p.adj[ob + j];
+        const uint32_t ev = j == tid ? (v0 == u ? t : e0) : (uint32_t)p.E[v];
         const bool fire = p.ext ? (t < ev && cap >= ev) : ev > t;  // fastk.cpp:22-24
         if (!fire) continue;
         ++f;
