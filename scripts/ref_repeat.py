@@ -8,12 +8,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--hybrid", type=int, default=1)
+ap.add_argument("--alternate", action="store_true", help="alternate hybrid_tail off / on")
 a = ap.parse_args()
 desc, (p0, p1, p2), seed = CONFIGS[a.config]
 g = K.GpuGraph(K.gen_config(a.config, p0, p1, p2, seed=seed))
 seen = collections.Counter()
-for _ in range(a.reps):
-    core, st = g.solve(K.FastKOptions(rule=K.Rule.REFERENCE, hybrid_tail=bool(a.hybrid)))
-    seen[(st["iterations"], st["messages_sent"], st["messages_drained"], st["tail_pops"])] += 1
+for i in range(a.reps):
+    hyb = bool(i & 1) if a.alternate else bool(a.hybrid)
+    core, st = g.solve(K.FastKOptions(rule=K.Rule.REFERENCE, hybrid_tail=hyb))
+    seen[(hyb, st["iterations"], st["messages_sent"], st["messages_drained"], st["tail_pops"])] += 1
 for k, v in seen.items():
     print("cfg", a.config, "counters", k, "x", v)
