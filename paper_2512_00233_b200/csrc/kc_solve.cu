@@ -59,7 +59,10 @@ using namespace dev;
 // Active vertices grabbed per atomic, per class.
 constexpr uint32_t G_BIG = 2, G_WARP = 8, G_SUB = 32, G_THREAD = 32;
 constexpr uint32_t COMPACT_IDS = SOLVE_THREADS * 16;  // ids per CTA compaction block
-constexpr uint32_t CACHE_MIN_ACTIVE = 4096;  // smaller rounds skip the shared-memory cache
+#ifndef KC_SOLVE_CACHE_MIN
+#define KC_SOLVE_CACHE_MIN 4096
+#endif
+constexpr uint32_t CACHE_MIN_ACTIVE = KC_SOLVE_CACHE_MIN;  // smaller rounds skip the shared-memory cache
 
 template <typename OffT, typename EstT>
 struct P {
@@ -601,9 +604,14 @@ __device__ void notify_huge(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
                                 [&](uint32_t ok, const uint32_t(&ids)[8], const uint32_t(&x)[8]) {
                                   notify_batch<8>(p, rv, ok, ids, x, t, cap, acc);
                                 }, id_cut(p, t + 1), p.sorted);
-      if (tid == 0) p.E[u] = (EstT)t;  // apply (fastk.cpp:153)
     }
+    // Apply only after every thread of the CTA has read cap = E[u]: stream_row
+    // has no CTA barrier, so a warp that leaves its share of the row early
+    // (degree cut, `stop`) could otherwise store E[u] = t before a lagging
+    // warp's load, which then sees t >= cap and skips its share of the
+    // notifications (the rare `fires` / messages_sent deficit).
     __syncthreads();
+    if (tid == 0 && t < cap) p.E[u] = (EstT)t;  // apply (fastk.cpp:153)
   }
 }
 
