@@ -61,3 +61,23 @@ def test_clamped_start_hub_round_zero(gpu, oracle):
     assert np.array_equal(core_c, oracle.peel(g)) and np.array_equal(core_r, core_c)
     assert st_c["iterations"] == st_r["iterations"]
     assert st_c["h_graph"] < 30000
+
+
+def test_reference_rule_counters_repeatable(gpu, oracle):
+    """Hub notify (kc_solve.cu notify_huge) applies E[u] = t only after a CTA
+    barrier: with the degree cut a warp can finish its share of a hub row early,
+    and before the barrier its store could reach a lagging warp's cap = E[u]
+    load, which then skipped its notifications (a rare, timing-dependent
+    messages_sent deficit).  Repeated solves must give identical counters."""
+    for name, n, pairs in _graphs(oracle):
+        if name not in ("star_clique", "chunglu_hubs", "rmat15"):
+            continue
+        g = oracle.build_csr(n, pairs)
+        gg = gpu.GpuGraph(gpu.Graph(g.off, g.nbr))
+        o = gpu.FastKOptions(rule=gpu.Rule.REFERENCE, hybrid_tail=False)
+        first = None
+        for _ in range(25):
+            _, st = gg.solve(o)
+            rep = {k: st[k] for k in KEYS}
+            first = first or rep
+            assert rep == first, name
