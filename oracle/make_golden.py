@@ -186,9 +186,10 @@ def make_configs(which):
                "k_sum": int(core.astype(np.uint64).sum()), "h_graph": O.degree_hindex(g),
                "max_degree": int(np.diff(g.off).max()),
                "coreness_histogram": np.bincount(core).tolist()}
-        if cfg <= 3:  # the reference rule's work for the ref-equivalent GTEPS
-            j = O.jacobi(g, "ref_ext", clamp=True)
-            rec["jacobi_ref_ext"] = j["stats"]
+        # the reference rule's work for the ref-equivalent GTEPS (every config;
+        # cfg 4 / 5 take minutes of single-threaded replay)
+        j = O.jacobi(g, "ref_ext", clamp=True)
+        rec["jacobi_ref_ext"] = j["stats"]
         have[str(cfg)] = rec
         print(cfg, {k: v for k, v in rec.items() if k != "coreness_histogram"}, flush=True)
         with open(path, "w") as f:
@@ -247,6 +248,36 @@ def make_edge_lists():
         json.dump(out, f, indent=0)
 
 
+def add_full_counters(which):
+    """Both counter sets of a full-size config from ONE generation: the
+    Jacobi replay's reference-rule RunReport without the tail (what the GPU's
+    REFERENCE rule with hybrid_tail=false must reproduce) and the unmodified
+    reference kcore::fastk_run with its defaults.  The coreness of both is
+    checked against the committed peel digest."""
+    path = os.path.join(GOLDEN, "configs.json")
+    have = json.load(open(path))
+    for cfg in which:
+        n, pairs = gen(cfg)
+        g = O.build_csr(n, pairs)
+        del pairs
+        rec = have[str(cfg)]
+        assert sha(g.off) == rec["offsets_sha256"] and sha(g.nbr) == rec["neighbors_sha256"]
+        j = O.jacobi(g, "ref_ext", clamp=True)
+        assert sha(j["est"].astype(np.uint32)) == rec["coreness_sha256"]
+        rec["jacobi_ref_ext"] = j["stats"]
+        del j
+        print(cfg, "jacobi", rec["jacobi_ref_ext"], flush=True)
+        core, st = O.RefGraph(g).fastk(threads=O.physical_cores(), batch=256, ext=True, hybrid=True)
+        assert sha(core.astype(np.uint32)) == rec["coreness_sha256"]
+        rec["reference_fastk_default"] = {k: int(st[k]) for k in (
+            "iterations", "messages_sent", "messages_drained", "tail_pops")}
+        print(cfg, "reference", rec["reference_fastk_default"], flush=True)
+        have = json.load(open(path))
+        have[str(cfg)] = rec
+        with open(path, "w") as f:
+            json.dump(have, f, indent=1)
+
+
 def add_ref_counters(which):
     """RunReport of the unmodified reference kcore::fastk_run with its
     defaults (batch 256, extended notify, hybrid tail) on the full-size
@@ -271,6 +302,8 @@ if __name__ == "__main__":
     ap.add_argument("--configs", default="", help="comma list of config ids to digest")
     ap.add_argument("--no-small", action="store_true")
     ap.add_argument("--ref-counters", default="", help="comma list: add the reference's RunReport")
+    ap.add_argument("--full-counters", default="",
+                    help="comma list: Jacobi replay + reference RunReport (one generation)")
     ap.add_argument("--edge-lists", action="store_true", help="edge-list loader fixtures")
     a = ap.parse_args()
     O.build(ref=True)
@@ -280,5 +313,7 @@ if __name__ == "__main__":
         make_configs([int(x) for x in a.configs.split(",")])
     if a.ref_counters:
         add_ref_counters([int(x) for x in a.ref_counters.split(",")])
+    if a.full_counters:
+        add_full_counters([int(x) for x in a.full_counters.split(",")])
     if a.edge_lists:
         make_edge_lists()

@@ -28,7 +28,7 @@ def build(ref: bool = True) -> None:
     """Compile liboracle.so (and the reference when its sources are mounted)."""
     targets = ["oracle"]
     if ref and os.path.isdir(REF_SRC):
-        targets.append("ref")
+        targets += ["ref", "ref_nofastk"]
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 
