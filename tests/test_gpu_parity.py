@@ -312,6 +312,8 @@ def test_full_size_configs_vs_golden(gpu, cfg):
         j = d["jacobi_ref_ext"]
         assert st2["iterations"] == j["iterations"]
         assert st2["messages_sent"] == j["messages_sent"]
+        assert st2["messages_drained"] == j["messages_drained"]
+        assert st2["tail_pops"] == 0
         assert st2["e_scan"] == j["e_scan"]
     if "reference_fastk_default" in d:  # the reference's defaults incl. the hybrid tail
         core3, st3 = gg.solve(gpu.FastKOptions(rule=gpu.Rule.REFERENCE))
