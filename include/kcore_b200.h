@@ -75,6 +75,7 @@ typedef struct kc_options {
 #define KC_DEBUG_PHASE_TIMES 1u /* record per-CTA per-round phase timestamps */
 #define KC_DEBUG_LEGACY_COUNT 2u /* counting rule on the flag-frontier solver (A/B) */
 #define KC_DEBUG_VERIFY_PERTURB 4u /* kc_verify self-test: candidate[u] += 1 for u % 997 == 0 */
+#define KC_DEBUG_NO_PULL 8u /* counting rule: push notify in round 0 (A/B of the pull phase) */
 
 /* RunReport (report.hpp:17-23) + work counters and timings. */
 typedef struct kc_stats {

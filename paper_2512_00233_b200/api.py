@@ -73,6 +73,7 @@ ABI_SYMBOLS = (
 KC_DEBUG_PHASE_TIMES = 1
 KC_DEBUG_LEGACY_COUNT = 2
 KC_DEBUG_VERIFY_PERTURB = 4
+KC_DEBUG_NO_PULL = 8
 KC_UPLOAD_FORCE_OFF64 = 1
 KC_UPLOAD_FORCE_EST32 = 2
 KC_UPLOAD_UNSORTED_ROWS = 4

@@ -202,6 +202,7 @@ void free_solver(kc_graph* g) {
   dfree(g->sb.rlen, g->stream);
   dfree(g->sb.rthr, g->stream);
   dfree(g->sb.spec, g->stream);
+  dfree(g->sb.pflag, g->stream);
   dfree(g->sb.lq[0], g->stream);
   dfree(g->sb.lq[1], g->stream);
   dfree(g->sb.flag[0], g->stream);
@@ -263,6 +264,8 @@ kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
     CK(dmalloc((void**)&b.lq[ph], ((size_t)b.cls_begin[1] + 1) * sizeof(uint32_t), g->stream));
     CK(cudaMemsetAsync(b.lq[ph], 0xff, ((size_t)b.cls_begin[1] + 1) * sizeof(uint32_t), g->stream));
   }
+  CK(dmalloc((void**)&b.pflag, n_pad, g->stream));
+  CK(cudaMemsetAsync(b.pflag, 0, n_pad, g->stream));
   CK(dmalloc((void**)&b.flag[0], n_pad, g->stream));
   CK(dmalloc((void**)&b.flag[1], n_pad, g->stream));
   CK(cudaMemsetAsync(b.est[0], 0, n_pad * es, g->stream));
@@ -339,6 +342,7 @@ kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_
   c.max_rounds = o.max_rounds;
   c.tail_threshold = tail_switch ? o.batch : 0u;
   c.num_sms = g->num_sms;
+  c.pull = (o.reserved[0] & KC_DEBUG_NO_PULL) ? 0u : 1u;
   if (uses_count_kernel(o))
     CK(launch_count_rounds(g->sb, c, g->est16, g->lay.off64, r_begin, r_end, g->stream));
   else

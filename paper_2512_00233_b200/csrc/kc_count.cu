@@ -154,6 +154,7 @@ struct CP {
   uint32_t* spec_r;     // speculative next-round evaluation: round it is valid for,
   uint32_t* spec_t;     //   its level and
   uint32_t* spec_c;     //   count(>= level) (computed by the notify scan, see NOTIFY)
+  uint8_t* pflag;       // PULL: round-1 droppers (compacted into round 1's queue)
   DegCut dc;
   uint32_t n_nz;
   uint32_t cb[NCLS + 1];
@@ -168,6 +169,7 @@ struct CP {
   uint32_t* status;
   unsigned long long* prof;
   uint32_t r_begin, r_end, cache_n, clamp_drop;
+  bool pull;            // round 0 ends with the PULL phase (see the kernel)
 };
 
 template <typename EstT>
@@ -180,6 +182,7 @@ struct View {
   uint32_t* qnext;       // next round's queue
   uint32_t cache_n;      // ids cached in shared memory this phase (0: none)
   bool r0;
+  bool pull;             // the PULL phase: every vertex evaluated against N
   uint32_t round;
 };
 
@@ -552,7 +555,7 @@ struct Item {
 // A vertex with a list (thr != 0) is first evaluated on it: levels >= thr
 // are decided by the list alone.  Only if no level >= max(lo, thr)
 // qualifies does the CSR row get scanned.
-template <typename OffT, typename EstT>
+template <bool PULL, typename OffT, typename EstT>
 __device__ __forceinline__ Item eval_item(const CP<OffT, EstT>& p, const View<EstT>& v,
                                           const EstT* s_cache, uint32_t u) {
   Item it;
@@ -564,7 +567,7 @@ __device__ __forceinline__ Item eval_item(const CP<OffT, EstT>& p, const View<Es
   const uint64_t oe = p.off[u + 1];
   it.cap = est_at(s_cache, v.cache_n, v.snap, u);
   uint32_t lo = 0, thr = 0, sr = 0, st = 0, sc = 0, rl = 0;
-  if (!v.r0) {
+  if (!v.r0 && !PULL) {
     lo = p.cnt[u];
     thr = p.rthr[u];
     sr = p.spec_r[u];
@@ -574,7 +577,7 @@ __device__ __forceinline__ Item eval_item(const CP<OffT, EstT>& p, const View<Es
   }
   it.deg = (uint32_t)(oe - it.ob);
   it.lo = lo;
-  const bool big = !v.r0 && it.deg > LIST_MIN_DEG;
+  const bool big = !v.r0 && !PULL && it.deg > LIST_MIN_DEG;
   it.thr = big ? thr : 0u;
   it.list = it.thr != 0;
   it.spec = big && sr == v.round;
@@ -596,9 +599,20 @@ __device__ __forceinline__ Item eval_item(const CP<OffT, EstT>& p, const View<Es
   return it;
 }
 
-template <typename OffT, typename EstT, typename A>
-__device__ __forceinline__ void finish_eval(const CP<OffT, EstT>& p, const Item& it, uint32_t t,
-                                            uint32_t c, uint32_t scanned, A& acc) {
+template <bool PULL, typename OffT, typename EstT, typename A>
+__device__ __forceinline__ void finish_eval(const CP<OffT, EstT>& p, const View<EstT>& v,
+                                            const Item& it, uint32_t t, uint32_t c,
+                                            uint32_t scanned, A& acc) {
+  if (PULL) {  // PULL (see the kernel): round 1's evaluation, round 0's apply
+    acc.nscan += scanned;
+    p.cnt[it.u] = c;
+    p.E[it.u] = (EstT)it.cap;  // E <- N (fastk.cpp:153); N is read by others this phase
+    if (t < it.cap) {
+      p.spec_t[it.u] = t;      // N <- t by the compaction, after the barrier
+      p.pflag[it.u] = 1;
+    }
+    return;
+  }
   acc.evals += 1;
   acc.escan += it.deg;
   acc.ascan += scanned;
@@ -614,17 +628,17 @@ __device__ __forceinline__ void finish_eval(const CP<OffT, EstT>& p, const Item&
 }
 
 
-template <typename OffT, typename EstT, typename A>
+template <bool PULL, typename OffT, typename EstT, typename A>
 __device__ __forceinline__ void eval_warp(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                           uint32_t* bins, const Item& it, A& acc) {
   if (it.spec) {
-    if (lane_id() == 0) finish_eval(p, it, it.spec_t, it.spec_c, 0u, acc);
+    if (lane_id() == 0) finish_eval<PULL>(p, v, it, it.spec_t, it.spec_c, 0u, acc);
     return;
   }
   if (KC_R0_SORTED && v.r0 && p.dc.sorted) {
     uint32_t scanned = 0;
     const uint2 tc = r0_sorted_warp(p.adj, p.dc.t, it.ob, it.deg, it.cap, scanned);
-    if (lane_id() == 0) finish_eval(p, it, tc.x, tc.y, scanned, acc);
+    if (lane_id() == 0) finish_eval<PULL>(p, v, it, tc.x, tc.y, scanned, acc);
     return;
   }
   const EstT* snap = v.snap;
@@ -633,7 +647,7 @@ __device__ __forceinline__ void eval_warp(const CP<OffT, EstT>& p, const View<Es
   if (KC_R0_PASSA && v.r0) {
     const uint32_t cA = warp_count_ge(p.adj, snap, s_cache, cache_n, it.ob, it.ob + it.deg, it.cap);
     if (cA >= it.cap) {
-      if (lane_id() == 0) finish_eval(p, it, it.cap, cA, it.deg, acc);
+      if (lane_id() == 0) finish_eval<PULL>(p, v, it, it.cap, cA, it.deg, acc);
       return;
     }
     lo = cA;  // count(>= cA) >= count(>= cap) = cA: the answer is >= cA
@@ -650,15 +664,15 @@ __device__ __forceinline__ void eval_warp(const CP<OffT, EstT>& p, const View<Es
     scanned += len;
     if (tc.x != 0) break;  // found (a list miss falls through to the row)
   }
-  if (lane_id() == 0) finish_eval(p, it, tc.x, tc.y, scanned, acc);
+  if (lane_id() == 0) finish_eval<PULL>(p, v, it, tc.x, tc.y, scanned, acc);
 }
 
-template <typename OffT, typename EstT>
+template <bool PULL, typename OffT, typename EstT>
 __device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                          uint32_t* s_hist, Shared& sh, uint32_t u, Acc& acc) {
-  const Item it = eval_item(p, v, s_cache, u);
+  const Item it = eval_item<PULL>(p, v, s_cache, u);
   if (it.spec) {
-    if (threadIdx.x == 0) finish_eval(p, it, it.spec_t, it.spec_c, 0u, acc);
+    if (threadIdx.x == 0) finish_eval<PULL>(p, v, it, it.spec_t, it.spec_c, 0u, acc);
     __syncthreads();
     return;
   }
@@ -675,7 +689,7 @@ __device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>&
                                     });
     const uint32_t cA = block_sum(c, sh.red);
     if (cA >= it.cap) {
-      if (threadIdx.x == 0) finish_eval(p, it, it.cap, cA, it.deg, acc);
+      if (threadIdx.x == 0) finish_eval<PULL>(p, v, it, it.cap, cA, it.deg, acc);
       __syncthreads();
       return;
     }
@@ -695,7 +709,7 @@ __device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>&
                      lo, it.deg, !v.r0, sh.out, p.dc);
     scanned += it.deg;
   }
-  if (threadIdx.x == 0) finish_eval(p, it, sh.out[0], sh.out[1], scanned, acc);
+  if (threadIdx.x == 0) finish_eval<PULL>(p, v, it, sh.out[0], sh.out[1], scanned, acc);
   __syncthreads();
 }
 
@@ -771,12 +785,12 @@ __device__ void consume_long(const CP<OffT, EstT>& p, const View<EstT>& v, Share
 
 // WARP and BIG classes: warp per vertex; metadata of a grab loaded one lane
 // per item, then walked.
-template <typename OffT, typename EstT, typename A>
+template <bool PULL, typename OffT, typename EstT, typename A>
 __device__ __forceinline__ void eval_wclass_impl(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                             uint32_t* bins, int c, uint32_t gmax, A& acc) {
   for_class(p, v, c, gmax, [&](uint32_t u, uint32_t n) {
     Item mine{};
-    if (lane_id() < n) mine = eval_item(p, v, s_cache, u);
+    if (lane_id() < n) mine = eval_item<PULL>(p, v, s_cache, u);
     for (uint32_t i = 0; i < n; ++i) {
       Item it;
       it.u = __shfl_sync(FULL, mine.u, i);
@@ -790,18 +804,18 @@ __device__ __forceinline__ void eval_wclass_impl(const CP<OffT, EstT>& p, const 
       it.spec = __shfl_sync(FULL, (uint32_t)mine.spec, i) != 0;
       it.spec_t = __shfl_sync(FULL, mine.spec_t, i);
       it.spec_c = __shfl_sync(FULL, mine.spec_c, i);
-      eval_warp(p, v, s_cache, bins, it, acc);
+      eval_warp<PULL>(p, v, s_cache, bins, it, acc);
     }
   });
 }
 
 // Counters in registers for the whole phase (an Acc& into the kernel's
 // frame would be local-memory traffic per evaluation).
-template <typename OffT, typename EstT>
+template <bool PULL, typename OffT, typename EstT>
 __device__ __noinline__ void eval_wclass(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                             uint32_t* bins, int c, uint32_t gmax, Acc& acc) {
   Acc32 a{0, 0, 0, 0, 0, 0, false};
-  eval_wclass_impl(p, v, s_cache, bins, c, gmax, a);
+  eval_wclass_impl<PULL>(p, v, s_cache, bins, c, gmax, a);
   merge_acc(acc, a);
 }
 
@@ -890,13 +904,13 @@ __device__ __forceinline__ void flat_eval_impl(const CP<OffT, EstT>& p, const Vi
     Item it{};
     uint32_t L = 0;
     if (lane < n) {
-      it = eval_item(p, v, s_cache, u);
+      it = eval_item<false>(p, v, s_cache, u);
       L = it.lo;
       if (it.list && it.thr > L) L = it.thr;
       if (it.cap > fb && it.cap - fb > L) L = it.cap - fb;
       if (L < 1u) L = 1u;
     }
-    if (lane < n && it.spec) finish_eval(p, it, it.spec_t, it.spec_c, 0u, acc);
+    if (lane < n && it.spec) finish_eval<false>(p, v, it, it.spec_t, it.spec_c, 0u, acc);
     const bool pending = lane < n && !it.spec;
     const uint32_t len = pending ? it.len : 0u;
     const uint32_t incl = warp_incl_scan(len);
@@ -934,7 +948,7 @@ __device__ __forceinline__ void flat_eval_impl(const CP<OffT, EstT>& p, const Vi
           break;
         }
       }
-      if (t) finish_eval(p, it, t, run, it.len, acc);
+      if (t) finish_eval<false>(p, v, it, t, run, it.len, acc);
       else deep = true;  // below the window: per-vertex passes
     }
     uint32_t dm = __ballot_sync(FULL, deep);
@@ -952,7 +966,7 @@ __device__ __forceinline__ void flat_eval_impl(const CP<OffT, EstT>& p, const Vi
       d.ob = __shfl_sync(FULL, it.ob, i);
       d.list = __shfl_sync(FULL, (uint32_t)it.list, i) != 0;
       d.spec = false;
-      eval_warp(p, v, s_cache, bins, d, acc);
+      eval_warp<false>(p, v, s_cache, bins, d, acc);
     }
   });
 }
@@ -970,7 +984,7 @@ __device__ __noinline__ void flat_eval(const CP<OffT, EstT>& p, const View<EstT>
 // bisection on [lo, cap).
 // Round 0 on sorted rows (s_dcut: the cut table's first DEG_SUB_MAX + 2
 // entries in shared memory) takes r0_sorted_warp's rule: no gathers.
-template <typename OffT, typename EstT, typename A>
+template <bool PULL, typename OffT, typename EstT, typename A>
 __device__ __forceinline__ void eval_sub_impl(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                          const uint32_t* s_dcut, A& acc) {
   constexpr int R = DEG_SUB_MAX / 8;
@@ -987,7 +1001,7 @@ __device__ __forceinline__ void eval_sub_impl(const CP<OffT, EstT>& p, const Vie
       mob = p.off[mu];
       mdeg = (uint32_t)(p.off[mu + 1] - mob);
       mcap = est_at(s_cache, cache_n, snap, mu);
-      mlo = r0 ? 0u : p.cnt[mu];
+      mlo = (r0 || PULL) ? 0u : p.cnt[mu];
     }
     for (uint32_t i0 = 0; i0 < n; i0 += 4) {
       // every lane runs the shuffles; tiles beyond n idle
@@ -1023,7 +1037,7 @@ __device__ __forceinline__ void eval_sub_impl(const CP<OffT, EstT>& p, const Vie
           if (has && k == 0) {
             Item it;
             it.u = u; it.cap = cap; it.deg = deg; it.len = deg; it.thr = 0;
-            finish_eval(p, it, t, t ? c : deg, deg, acc);
+            finish_eval<PULL>(p, v, it, t, t ? c : deg, deg, acc);
           }
           continue;
         }
@@ -1046,17 +1060,17 @@ __device__ __forceinline__ void eval_sub_impl(const CP<OffT, EstT>& p, const Vie
       if (has && k == 0) {
         Item it;
         it.u = u; it.cap = cap; it.deg = deg; it.len = deg; it.thr = 0;
-        finish_eval(p, it, t, c, deg, acc);
+        finish_eval<PULL>(p, v, it, t, c, deg, acc);
       }
     }
   });
 }
 
-template <typename OffT, typename EstT>
+template <bool PULL, typename OffT, typename EstT>
 __device__ __noinline__ void eval_sub(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                          const uint32_t* s_dcut, Acc& acc) {
   Acc32 a{0, 0, 0, 0, 0, 0, false};
-  eval_sub_impl(p, v, s_cache, s_dcut, a);
+  eval_sub_impl<PULL>(p, v, s_cache, s_dcut, a);
   merge_acc(acc, a);
 }
 
@@ -1109,7 +1123,7 @@ __device__ __forceinline__ void for_class_lanes(const CP<OffT, EstT>& p, const V
   }
 }
 
-template <typename OffT, typename EstT, typename A>
+template <bool PULL, typename OffT, typename EstT, typename A>
 __device__ __forceinline__ void eval_thread_impl(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                             const uint32_t* s_dcut, A& acc) {
   constexpr int R = DEG_THREAD_MAX;
@@ -1147,7 +1161,7 @@ __device__ __forceinline__ void eval_thread_impl(const CP<OffT, EstT>& p, const 
         for (int j = 0; j < R; ++j) c += x[k][j] < ct;
         Item it;
         it.u = u[k]; it.cap = cap[k]; it.deg = deg[k]; it.len = deg[k]; it.thr = 0;
-        finish_eval(p, it, t, t ? c : deg[k], deg[k], acc);
+        finish_eval<PULL>(p, v, it, t, t ? c : deg[k], deg[k], acc);
       }
       return;
     }
@@ -1174,16 +1188,16 @@ __device__ __forceinline__ void eval_thread_impl(const CP<OffT, EstT>& p, const 
       for (int j = 0; j < R; ++j) c += x[k][j] >= t;
       Item it;
       it.u = u[k]; it.cap = cap[k]; it.deg = deg[k]; it.len = deg[k]; it.thr = 0;
-      finish_eval(p, it, t, t ? c : deg[k], deg[k], acc);
+      finish_eval<PULL>(p, v, it, t, t ? c : deg[k], deg[k], acc);
     }
   });
 }
 
-template <typename OffT, typename EstT>
+template <bool PULL, typename OffT, typename EstT>
 __device__ __noinline__ void eval_thread(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                             const uint32_t* s_dcut, Acc& acc) {
   Acc32 a{0, 0, 0, 0, 0, 0, false};
-  eval_thread_impl(p, v, s_cache, s_dcut, a);
+  eval_thread_impl<PULL>(p, v, s_cache, s_dcut, a);
   merge_acc(acc, a);
 }
 
@@ -1744,6 +1758,105 @@ __device__ __forceinline__ void flush_acc(const CP<OffT, EstT>& p, uint32_t sr, 
   }
 }
 
+// The EVALUATE phase (every class; the long-scan queue of slot `ph`), inline
+// in the kernel body; its PULL instance runs out of line (pull_phase).
+template <bool PULL, typename OffT, typename EstT>
+__device__ __forceinline__ void eval_phase(const CP<OffT, EstT>& p, const View<EstT>& v, Shared& sh,
+                                        Ctl& ctl, int ph, const EstT* s_cache, uint32_t* s_hist,
+                                        uint32_t* w_bins, FlatW& fw, const uint32_t* s_dcut,
+                                        unsigned long long* pf, Acc& acc) {
+  auto eval_long = [&](uint32_t u) { eval_cta<PULL>(p, v, s_cache, s_hist, sh, u, acc); };
+  huge_warps(p, v, sh, ctl, ph, [&](uint32_t u) {
+    const Item it = eval_item<PULL>(p, v, s_cache, u);  // metadata loaded once
+    // (round 0 on sorted rows reads a prefix only: always a warp's)
+    if (it.len > WARP_MAX_LEN && !(KC_R0_SORTED && v.r0 && p.dc.sorted)) return false;
+    eval_warp<PULL>(p, v, s_cache, w_bins, it, acc);
+    return true;
+  });
+  consume_long(p, v, sh, ctl, ph, false, eval_long);
+  if (pf) pf[2] = gtimer();
+  if (v.r0 || PULL || !KC_FLAT_EVAL) {
+    eval_wclass<PULL>(p, v, s_cache, w_bins, C_BIG, GMAX_BIG, acc);
+    eval_wclass<PULL>(p, v, s_cache, w_bins, C_WARP, GMAX_WARP, acc);
+  } else {
+    flat_eval(p, v, s_cache, w_bins, fw, C_BIG, GMAX_BIG, acc);
+    flat_eval(p, v, s_cache, w_bins, fw, C_WARP, GMAX_WARP, acc);
+  }
+  if (pf) pf[3] = gtimer();
+  eval_sub<PULL>(p, v, s_cache, s_dcut, acc);
+  eval_thread<PULL>(p, v, s_cache, s_dcut, acc);
+  consume_long(p, v, sh, ctl, ph, true, eval_long);
+  if (pf) pf[4] = gtimer();
+}
+
+template <typename OffT, typename EstT>
+__device__ __noinline__ void pull_phase(const CP<OffT, EstT>& p, const View<EstT>& v, Shared& sh,
+                                        Ctl& ctl, const EstT* s_cache, uint32_t* s_hist,
+                                        uint32_t* w_bins, FlatW& fw, const uint32_t* s_dcut,
+                                        Acc& acc) {
+  eval_phase<true>(p, v, sh, ctl, 1, s_cache, s_hist, w_bins, fw, s_dcut,
+                   (unsigned long long*)nullptr, acc);
+}
+
+// After PULL: the flagged round-1 droppers become round 1's queue (class
+// segments, ids ascending within a CTA block), their new level moves from
+// spec_t into N, and round 1's evaluation counters are added.  CTAs take
+// interleaved blocks of PULL_IDS ids; each thread reads 16 flags with one
+// 128-bit load; one block scan and one atomicAdd per CTA block.
+constexpr uint32_t PULL_IDS = SOLVE_THREADS * 16;
+
+template <typename OffT, typename EstT>
+__device__ __noinline__ void compact_pull(const CP<OffT, EstT>& p, uint32_t* qcnt, uint32_t* queue,
+                             Shared& sh, RoundStat& st) {
+  const uint32_t tid = threadIdx.x;
+  unsigned long long evals = 0, escan = 0;
+  for (int c = 0; c < NCLS; ++c) {
+    const uint32_t b0 = p.cb[c], b1 = p.cb[c + 1];
+    const uint32_t a0 = b0 & ~15u;
+    const uint32_t nblk = (b1 - a0 + PULL_IDS - 1) / PULL_IDS;
+    for (uint32_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+      const uint32_t a = a0 + blk * PULL_IDS + 16 * tid;
+      uint4 w = make_uint4(0, 0, 0, 0);
+      if (a < b1) w = *reinterpret_cast<const uint4*>(p.pflag + a);
+      uint32_t m = 0;  // bit j: id a+j dropped and inside the class
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t word = j < 4 ? w.x : j < 8 ? w.y : j < 12 ? w.z : w.w;
+        const uint32_t id = a + j;
+        if ((word >> (8 * (j & 3)) & 0xffu) && id >= b0 && id < b1) m |= 1u << j;
+      }
+      const uint32_t mine = __popc(m);
+      const uint32_t off = block_excl_scan(mine, sh.red);
+      if (tid == SOLVE_THREADS - 1) {
+        const uint32_t tot = off + mine;
+        sh.item = tot ? atomicAdd(&qcnt[c], tot) : 0u;
+      }
+      __syncthreads();
+      uint32_t pos = b0 + sh.item + off;
+      __syncthreads();
+      if (m) {
+#pragma unroll 1
+        for (int j = 0; j < 16; ++j)
+          if (m >> j & 1) {
+            const uint32_t u = a + j;
+            queue[pos++] = u;
+            p.pflag[u] = 0;
+            p.N[u] = (EstT)p.spec_t[u];
+            evals += 1;
+            escan += (uint64_t)(p.off[u + 1] - p.off[u]);
+          }
+      }
+    }
+  }
+  evals = __reduce_add_sync(FULL, (uint32_t)evals);
+  for (int d = 16; d > 0; d >>= 1) escan += __shfl_xor_sync(FULL, escan, d);
+  if (lane_id() == 0 && evals) {
+    atomicAdd(&st.evals, evals);
+    atomicAdd(&st.drops, evals);
+    atomicAdd(&st.escan, escan);
+  }
+}
+
 template <typename OffT, typename EstT>
 __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __grid_constant__ CP<OffT, EstT> p) {
   cg::grid_group grid = cg::this_grid();
@@ -1772,6 +1885,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
   if (lane_id() < NCLS) wn[lane_id()] = 0;
   if (tid < DEG_SUB_MAX + 2) s_dcut[tid] = p.dc.at(tid);
   __syncthreads();
+  bool evaluated = false;  // this round's evaluation already ran (PULL did round 1's)
 
   for (uint32_t r = p.r_begin; r < p.r_end; ++r) {
     const uint32_t cur = r & 1, nxt = cur ^ 1;
@@ -1790,6 +1904,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     q.qn = vl.qn;
     q.qnext = vl.qnext;
     vl.r0 = r == 0;
+    vl.pull = false;
     vl.round = r;
     unsigned long long* pf = (p.prof && r < PROF_ROUNDS && tid == 0)
                                  ? p.prof + ((size_t)r * gridDim.x + blockIdx.x) * PROF_PHASES
@@ -1823,41 +1938,23 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     if (tid == 0) sh.drop = 0;
     const uint32_t cache_n = active >= CACHE_MIN_ACTIVE ? p.cache_n : 0u;
     vl.cache_n = cache_n;
-    if (cache_n) fill_cache(s_cache, (const EstT*)p.E, cache_n);
+    if (cache_n && !evaluated) fill_cache(s_cache, (const EstT*)p.E, cache_n);
     if (tid == 0) s_view = vl;
     __syncthreads();
     Acc acc{0, 0, 0, 0, 0, 0, false};
     if (pf) pf[1] = gtimer();
     // ---------------- EVALUATE ----------------
     Ctl& ctl = p.ctl[cur];
-    auto eval_long = [&](uint32_t u) { eval_cta(p, v, s_cache, s_hist, sh, u, acc); };
-    huge_warps(p, v, sh, ctl, 0, [&](uint32_t u) {
-      const Item it = eval_item(p, v, s_cache, u);  // metadata loaded once
-      // (round 0 on sorted rows reads a prefix only: always a warp's)
-      if (it.len > WARP_MAX_LEN && !(KC_R0_SORTED && v.r0 && p.dc.sorted)) return false;
-      eval_warp(p, v, s_cache, w_bins, it, acc);
-      return true;
-    });
-    consume_long(p, v, sh, ctl, 0, false, eval_long);
-    if (pf) pf[2] = gtimer();
-    if (v.r0 || !KC_FLAT_EVAL) {
-      eval_wclass(p, v, s_cache, w_bins, C_BIG, GMAX_BIG, acc);
-      eval_wclass(p, v, s_cache, w_bins, C_WARP, GMAX_WARP, acc);
-    } else {
-      flat_eval(p, v, s_cache, w_bins, s_flat[warp_id()], C_BIG, GMAX_BIG, acc);
-      flat_eval(p, v, s_cache, w_bins, s_flat[warp_id()], C_WARP, GMAX_WARP, acc);
-    }
-    if (pf) pf[3] = gtimer();
-    eval_sub(p, v, s_cache, s_dcut, acc);
-    eval_thread(p, v, s_cache, s_dcut, acc);
-    consume_long(p, v, sh, ctl, 0, true, eval_long);
-    if (pf) pf[4] = gtimer();
+    if (!evaluated) {
+    eval_phase<false>(p, v, sh, ctl, 0, s_cache, s_hist, w_bins, s_flat[warp_id()], s_dcut, pf, acc);
     if (v.r0) {
       if (__any_sync(FULL, acc.any_drop) && lane_id() == 0) sh.drop = 1;
       __syncthreads();
       if (tid == 0 && sh.drop) p.anydrop[0] = 1;
     }
     grid.sync();
+    }  // !evaluated
+    evaluated = false;
     // The reference starts at est = deg (fastk.cpp:67-68); the solver starts
     // at min(deg, H), so round 0 "changed" also when some degree exceeds H
     // (that drop is already applied).  Keeps iterations equal to the reference.
@@ -1872,6 +1969,42 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
       return;
     }
     if (pf) pf[5] = gtimer();
+    if (v.r0 && p.pull) {
+      // ---------------- PULL (round 0's notify + round 1's evaluate) ----------------
+      // Round 1's snapshot is N (round 0's settled levels).  Instead of every
+      // round-0 dropper pushing counter decrements to its neighbours (one
+      // atomic per fire: 176 M on R-MAT 26) and round 1 then evaluating the
+      // vertices the decrements activated, every vertex evaluates itself
+      // against N once: cap = N[v], t = capped h-index over N, c = count(N
+      // >= t).  cnt[v] = c is exactly the counter the decrements would have
+      // left (count(N >= N[v]) when v does not drop) or round 1's evaluation
+      // stores; a vertex drops (t < cap) iff its counter would have crossed
+      // below N[v], i.e. iff round 0's notify would have activated it.  So
+      // the Jacobi trajectory, the evaluations (V_eval, E_scan) and round 1's
+      // queue are unchanged; only round 0's push (and its decrements) goes.
+      // The apply E[v] = N[v] is done here; the new levels wait in spec_t
+      // until the compaction (N is being read).
+      vl.snap = p.N;
+      vl.grab = p.ctl[cur].grab2;
+      vl.r0 = false;
+      vl.pull = true;
+      if (cache_n) fill_cache(s_cache, (const EstT*)p.N, cache_n);
+      if (tid == 0) s_view = vl;
+      __syncthreads();
+      if (pf) pf[6] = gtimer();
+      pull_phase(p, v, sh, ctl, s_cache, s_hist, w_bins, s_flat[warp_id()], s_dcut, acc);
+      flush_acc(p, sr, acc, sh.acc);
+      grid.sync();
+      compact_pull(p, p.ctl[nxt].qcnt, p.queue[nxt], sh, p.stats[1 < STAT_SLOTS - 1 ? 1 : STAT_SLOTS - 1]);
+      grid.sync();
+      if (pf) pf[7] = gtimer();
+      if (blockIdx.x == 0 && tid == 0) {
+        p.status[0] = r + 1;
+        p.status[3] = 0;
+      }
+      evaluated = true;  // round 1 starts at its notify phase
+      continue;
+    }
     // ---------------- NOTIFY + APPLY ----------------
     vl.snap = p.N;
     vl.grab = p.ctl[cur].grab2;
@@ -1965,6 +2098,7 @@ CP<OffT, EstT> make_params(const SolveBuffers& b) {
   p.spec_r = b.spec;
   p.spec_t = b.spec + n_pad;
   p.spec_c = b.spec + 2 * n_pad;
+  p.pflag = b.pflag;
   p.n_nz = b.n_nz;
   for (int c = 0; c <= NCLS; ++c) p.cb[c] = b.cls_begin[c];
   p.E = static_cast<EstT*>(b.est[0]);
@@ -1990,6 +2124,7 @@ cudaError_t launch_t(const SolveBuffers& b, const SolveConfig& c, uint32_t r_beg
   p.r_end = r_end;
   p.cache_n = c.cache_n;
   p.clamp_drop = c.clamp_drop;
+  p.pull = c.pull && r_begin == 0 && r_end >= 2;
   const size_t smem = (((size_t)c.cache_n * sizeof(EstT) + 15) & ~(size_t)15) +
                       ((size_t)HREG + (size_t)NWARPS * NCLS * WQ) * sizeof(uint32_t);
   auto kern = count_rounds_kernel<OffT, EstT>;

@@ -73,6 +73,8 @@ struct SolveBuffers {
   uint32_t* rlen;            // counting rule: list lengths [n_pad]
   void* rthr;                // counting rule: list thresholds (EstT) [n_pad]
   uint32_t* lq[2];           // counting rule: long-scan queues per phase [cls_begin[1]]
+  uint8_t* pflag;            // counting rule: round-1 droppers found by the pull phase [n_pad]
+                             // (zero between solves: the compaction clears what it takes)
   uint32_t* spec;            // counting rule: next-round evaluations [3][n_pad16]
                              // (round tag, level, count), n_pad16 = n_nz rounded to 16
   Ctl* ctl;                  // [2]
@@ -99,6 +101,8 @@ struct SolveConfig {
                              // starts with fewer active vertices (the batch, fastk.hpp:29-31)
                              // and leave the rest to the sequential tail (0 = off)
   int num_sms;
+  uint32_t pull;             // counting rule: round 0's notify + round 1's evaluate as one
+                             // pull phase (kc_count.cu PULL) when the launch covers rounds 0-1
 };
 
 // Launch rounds [r_begin, r_end) of the persistent solver on `stream`.

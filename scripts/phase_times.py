@@ -10,16 +10,18 @@ ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--scale", type=int, default=0)
 ap.add_argument("--rule", type=int, default=2)
 ap.add_argument("--cache", type=int, default=0)
+ap.add_argument("--debug-flags", type=int, default=0, help="extra KC_DEBUG_* bits (e.g. 8: no pull)")
 a = ap.parse_args()
 desc, (p0, p1, p2), seed = CONFIGS[a.config]
 if a.scale: p0 = a.scale
 d = K.gen_config(a.config, p0, p1, p2, seed=seed)
 g = K.GpuGraph(d)
 o = K.FastKOptions(rule=K.Rule(a.rule), smem_cache=a.cache)
+o.debug_flags = a.debug_flags
 g.solve(o)
 core, st = g.solve(o)
 print("plain solve ms", st["t_solve_ms"], "iters", st["iterations"])
-o.debug_flags = KC_DEBUG_PHASE_TIMES
+o.debug_flags = KC_DEBUG_PHASE_TIMES | a.debug_flags
 core, st = g.solve(o)
 print("instrumented solve ms", st["t_solve_ms"])
 pt = g.phase_times().astype(np.int64)
