@@ -117,8 +117,13 @@ constexpr int WQ = KC_WQ;          // per-warp, per-class enqueue buffer (flushe
 #define KC_CUT_EVAL 1              // windowed evaluations skip / stop at ids below their floor
 #endif
 #ifndef KC_CUT_NOTIFY
-#define KC_CUT_NOTIFY 0            // notify row scans likewise, in their own function (R-MAT 26 -2.5%,
-                                   // R-MAT 22 +0.6%, Chung-Lu +1.1%: off)
+#define KC_CUT_NOTIFY 1            // notify row scans likewise, in their own function
+#endif
+#ifndef KC_ROW_FLOOR_BUILD
+#define KC_ROW_FLOOR_BUILD 1       // a row scan that builds a list resolves its next-round
+                                   // window only down to the list threshold L (a level below L
+                                   // needs the row again anyway), so the scan needs no value
+                                   // below L and on sorted rows stops at the degree cut dcut[L]
 #endif
 #ifndef KC_CUT_LISTS
 #define KC_CUT_LISTS 1             // ... also on (unsorted) lists: mask only
@@ -1394,7 +1399,7 @@ __device__ __noinline__ uint32_t notify_row_warp(const CP<OffT, EstT>& p, const 
                                                  uint32_t len, uint32_t t, uint32_t cap,
                                                  uint32_t build, uint32_t tag) {
   return notify_warp<true>(p, q, s_cache, cache_n, bins, p.adj, true, u, ob, len, t, cap, build,
-                           tag, 1u);
+                           tag, KC_ROW_FLOOR_BUILD && build ? build : 1u);
 }
 
 template <typename OffT, typename EstT>
@@ -2018,7 +2023,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
           d.thr ? notify_cta(p, q, s_cache, cache_n, sh, s_hist, p.radj, false, d.u, d.ob, d.len,
                              d.t, d.cap, 0u, KC_SPEC ? r + 1 : 0u, d.thr)
                 : notify_cta(p, q, s_cache, cache_n, sh, s_hist, p.adj, true, d.u, d.ob, d.len,
-                             d.t, d.cap, list_build(v.r0, d), KC_SPEC ? r + 1 : 0u, 1u);
+                             d.t, d.cap, list_build(v.r0, d), KC_SPEC ? r + 1 : 0u,
+                             KC_ROW_FLOOR_BUILD && list_build(v.r0, d) ? list_build(v.r0, d) : 1u);
       acc.fires += f;
       if (tid == 0) acc.nscan += d.len;
     };
