@@ -110,7 +110,7 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
 }
 
 template <bool RO>
-__device__ __forceinline__ uint4 ld_ids4(const uint32_t* src, uint64_t a) {
+__device__ __forceinline__ uint4 ld_ids4(const uint32_t* src, uint64_t a) {  // 4 ids at src + a
   uint4 r;
 #if KC_L2_STREAM_FIRST
   const uint64_t pol = l2_evict_first_policy();
@@ -287,80 +287,49 @@ __device__ __forceinline__ uint32_t tile8_sum(uint32_t v) {
 // Streaming over a row with 128-bit id loads: each of NT cooperating threads
 // takes 8 entries per step (two 16-byte loads, software-pipelined one step
 // ahead), gathers their 8 estimates, then hands (valid mask, ids, estimates)
-// to the callback.  Rows need not be 16-byte aligned: positions outside
-// [ob, oe) are masked (id arrays have ADJ_PAD spare entries).
-// ------------------------------------------------------------------------
-// `cut` / `stop`: as in stream_row_rt below.
-template <int NT, bool RO, typename EstT, typename F>
-__device__ __forceinline__ void stream_row(const uint32_t* src, const EstT* snap, uint32_t me,
-                                           uint64_t ob, uint64_t oe, const EstT* s_cache,
-                                           uint32_t cache_n, F&& f, uint32_t cut = 0xffffffffu,
-                                           bool stop = false) {
-  constexpr uint64_t STEP = (uint64_t)NT * 8;
-  uint64_t a = ob & ~(uint64_t)3;
-  uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-  if (a + 4 * me < oe) q0 = ld_ids4<RO>(src, a + 4 * me);
-  if (a + 4 * me + 4 * NT < oe) q1 = ld_ids4<RO>(src, a + 4 * me + 4 * NT);
-  for (; a < oe; a += STEP) {
-    uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
-    const uint64_t nb = a + STEP;
-    if (nb + 4 * me < oe) n0 = ld_ids4<RO>(src, nb + 4 * me);
-    if (nb + 4 * me + 4 * NT < oe) n1 = ld_ids4<RO>(src, nb + 4 * me + 4 * NT);
-    uint32_t ids[8], x[8];
-    uint32_t ok = 0;
-    bool past = false;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint64_t pos = a + 4 * me + (k >> 2) * 4 * NT + (k & 3);
-      ids[k] = u4_get(k < 4 ? q0 : q1, k & 3);
-      const bool in = pos >= ob && pos < oe;
-      const bool v = in && ids[k] < cut;
-      past |= in && !v;
-      ok |= (uint32_t)v << k;
-      x[k] = v ? est_at(s_cache, cache_n, snap, ids[k]) : 0u;
-    }
-    f(ok, ids, x);
-    if (stop && __any_sync(FULL, past)) break;
-    q0 = n0;
-    q1 = n1;
-  }
-}
-
-// Same stream with the load path chosen at run time (ro: immutable CSR rows
-// via the non-coherent path; else lists rewritten inside the kernel, L2
-// only) — one inlined copy serves both sources.
-__device__ __forceinline__ uint4 ld_ids4_rt(const uint32_t* src, uint64_t a, bool ro) {
-  return ro ? ld_ids4<true>(src, a) : ld_ids4<false>(src, a);
-}
-
+// to the callback.  Rows need not be 16-byte aligned: the stream starts at
+// the 16-byte granule holding ob and masks positions outside [ob, oe) (id
+// arrays have ADJ_PAD spare entries).  Position arithmetic is 32-bit,
+// relative to that granule (a row is < 2^32 entries): one 64-bit base.
 //
 // `cut`: ids >= cut are masked without a gather (with degree-descending ids,
 // id >= cut(x) means degree < x, so the estimate is < x too).  `stop`: the
 // source is sorted ascending, so once a warp's step holds an id >= cut every
 // later step of that warp does too — the warp leaves the stream.
+// `ro`: the immutable CSR via the non-coherent path; else lists rewritten
+// inside the kernel (L2 only).
+// ------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ld_ids4_rt(const uint32_t* p, bool ro) {
+  return ro ? ld_ids4<true>(p, 0) : ld_ids4<false>(p, 0);
+}
+
 template <int NT, typename EstT, typename F>
 __device__ __forceinline__ void stream_row_rt(const uint32_t* src, bool ro, const EstT* snap,
                                               uint32_t me, uint64_t ob, uint64_t oe,
                                               const EstT* s_cache, uint32_t cache_n, F&& f,
                                               uint32_t cut = 0xffffffffu, bool stop = false) {
-  constexpr uint64_t STEP = (uint64_t)NT * 8;
-  uint64_t a = ob & ~(uint64_t)3;
+  constexpr uint32_t STEP = (uint32_t)NT * 8;
+  const uint32_t* base = src + (ob & ~(uint64_t)3) + 4 * me;  // this thread's first granule
+  const uint32_t head = (uint32_t)(ob & 3);   // masked entries before the row
+  const uint32_t len = (uint32_t)(oe - ob);
+  const uint32_t end = head + len;            // relative end
+  const uint32_t l0 = 4 * me, l1 = 4 * me + 4 * NT;
   uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-  if (a + 4 * me < oe) q0 = ld_ids4_rt(src, a + 4 * me, ro);
-  if (a + 4 * me + 4 * NT < oe) q1 = ld_ids4_rt(src, a + 4 * me + 4 * NT, ro);
-  for (; a < oe; a += STEP) {
+  if (l0 < end) q0 = ld_ids4_rt(base, ro);
+  if (l1 < end) q1 = ld_ids4_rt(base + 4 * NT, ro);
+  for (uint32_t a = 0; a < end; a += STEP) {
     uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
-    const uint64_t nb = a + STEP;
-    if (nb + 4 * me < oe) n0 = ld_ids4_rt(src, nb + 4 * me, ro);
-    if (nb + 4 * me + 4 * NT < oe) n1 = ld_ids4_rt(src, nb + 4 * me + 4 * NT, ro);
+    const uint32_t nb = a + STEP;
+    if (nb + l0 < end) n0 = ld_ids4_rt(base + nb, ro);
+    if (nb + l1 < end) n1 = ld_ids4_rt(base + nb + 4 * NT, ro);
     uint32_t ids[8], x[8];
     uint32_t ok = 0;
     bool past = false;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const uint64_t pos = a + 4 * me + (k >> 2) * 4 * NT + (k & 3);
+      const uint32_t pos = a + (k < 4 ? l0 : l1) + (k & 3);
       ids[k] = u4_get(k < 4 ? q0 : q1, k & 3);
-      const bool in = pos >= ob && pos < oe;
+      const bool in = pos - head < len;  // head <= pos < end
       const bool v = in && ids[k] < cut;
       past |= in && !v;
       ok |= (uint32_t)v << k;
@@ -371,6 +340,15 @@ __device__ __forceinline__ void stream_row_rt(const uint32_t* src, bool ro, cons
     q0 = n0;
     q1 = n1;
   }
+}
+
+// The immutable CSR (RO) or a list, fixed at compile time.
+template <int NT, bool RO, typename EstT, typename F>
+__device__ __forceinline__ void stream_row(const uint32_t* src, const EstT* snap, uint32_t me,
+                                           uint64_t ob, uint64_t oe, const EstT* s_cache,
+                                           uint32_t cache_n, F&& f, uint32_t cut = 0xffffffffu,
+                                           bool stop = false) {
+  stream_row_rt<NT>(src, RO, snap, me, ob, oe, s_cache, cache_n, static_cast<F&&>(f), cut, stop);
 }
 
 // Round 0 on a degree-sorted row (`dcut`: the degree cut table, kc_count.cu
