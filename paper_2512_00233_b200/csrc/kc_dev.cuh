@@ -28,11 +28,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // Estimate of v: shared-memory cache for the highest-degree ids, global
 // (L1/L2) otherwise.  One generic load per gather keeps the inlined gather
 // sites small for the instruction cache.
+#ifndef KC_EST_CACHE
+#define KC_EST_CACHE 1   // 0: every gather from global memory (A/B: R-MAT 22 -1.5%,
+                         // R-MAT 26 +1.6%; explicit LDS/LDG pairs cost more)
+#endif
 template <typename EstT>
 __device__ __forceinline__ uint32_t est_at(const EstT* __restrict__ s_cache, uint32_t cache_n,
                                            const EstT* snap, uint32_t v) {
+#if KC_EST_CACHE
   const EstT* base = v < cache_n ? s_cache : snap;
   return (uint32_t)base[v];
+#else
+  (void)s_cache;
+  (void)cache_n;
+  __builtin_assume(__isGlobal(snap));
+  return (uint32_t)snap[v];
+#endif
 }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
