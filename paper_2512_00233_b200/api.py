@@ -281,6 +281,12 @@ class Graph:
             neighbors if neighbors is not None else np.zeros(0, np.uint32), dtype=np.uint32)
         if self._off.size < 1 or int(self._off[0]) != 0 or int(self._off[-1]) != self._nbr.size:
             raise ValueError("offsets must start at 0 and end at len(neighbors)")
+        # the reference's Graph cannot hold anything else (graph.hpp:37-75); the
+        # C-ABI re-checks on the device (KC_ERR_INVALID_ARGUMENT)
+        if self._off.size > 1 and bool(np.any(self._off[1:] < self._off[:-1])):
+            raise ValueError("offsets must be non-decreasing")
+        if self._nbr.size and int(self._nbr.max()) >= self._off.size - 1:
+            raise ValueError("neighbour id out of range")
 
     @classmethod
     def from_edges(cls, node_count: int, edges) -> "Graph":

@@ -30,19 +30,33 @@ thread_local std::string g_last_error;
 
 namespace kcb {
 cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t s) {
+  // the library's own pool per device (not the device's default pool: its
+  // release threshold is process-wide state other libraries rely on)
   static std::once_flag once[64];
+  static cudaMemPool_t pools[64];
   int dev = 0;
   cudaGetDevice(&dev);
   std::call_once(once[dev & 63], [dev] {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;  // keep freed blocks for the next solve
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      pools[dev & 63] = pool;
+    } else {
+      cudaGetLastError();
+      pools[dev & 63] = nullptr;  // fall back to the default pool, untouched
     }
   });
   static const bool dbg = std::getenv("KC_DEBUG_HOST") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
-  const cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 1, s);
+  cudaMemPool_t pool = pools[dev & 63];
+  const cudaError_t e = pool ? cudaMallocFromPoolAsync(p, bytes ? bytes : 1, pool, s)
+                             : cudaMallocAsync(p, bytes ? bytes : 1, s);
   if (dbg) {
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (ms > 0.5) std::fprintf(stderr, "[kc host] dmalloc %zu bytes: %.3f ms\n", bytes, ms);
@@ -438,6 +452,7 @@ struct HostClock {
 
 kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint32_t flags,
                         kc_graph** out) {
+  kcb::DeviceGuard device_guard;  // restore the caller's current device
   HostClock hc;
   if (!out) return fail(KC_ERR_INVALID_ARGUMENT, "out is null");
   *out = nullptr;
@@ -561,6 +576,10 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
     dfree(d_adj, g->stream);
   }
   if (e != cudaSuccess) return bail(cuda_fail(e, "layout"));
+  if (g->lay.invalid)
+    return bail(fail(KC_ERR_INVALID_ARGUMENT,
+                     "not a CSR: offsets must run 0..nnz non-decreasing and every neighbour id "
+                     "must be < n (graph.hpp:37-75)"));
   cudaEventElapsedTime(&g->t_upload, g->ev[0], g->ev[1]);
   cudaEventElapsedTime(&g->t_prep, g->ev[1], g->ev[2]);
   g->est16 = g->lay.h_graph < EST16_LIMIT && !(flags & KC_UPLOAD_FORCE_EST32);
@@ -622,6 +641,7 @@ kc_status kc_graph_upload_ex(const kc_csr_view* csr, int device, int on_device, 
 }
 
 void kc_graph_free(kc_graph* g) {
+  kcb::DeviceGuard device_guard;  // restore the caller's current device
   if (!g) return;
   HostClock hc;
   cudaSetDevice(g->device);
@@ -654,6 +674,7 @@ kc_status kc_graph_timings(const kc_graph* g, float* tu, float* tp) {
 
 static kc_status solve_impl(kc_graph* g, const kc_options* opt, uint32_t* out, bool out_dev,
                             kc_stats* st) {
+  kcb::DeviceGuard device_guard;  // restore the caller's current device
   g_last_error.clear();
   if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
   kc_options o;
@@ -791,6 +812,7 @@ kc_status boundary(kc_graph* g, Boundaries& b, uint64_t it, uint64_t active,
 
 kc_status observed_impl(kc_graph* g, const kc_options* opt, Boundaries& b, uint32_t* coreness,
                         kc_stats* st) {
+  kcb::DeviceGuard device_guard;  // restore the caller's current device
   g_last_error.clear();
   if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
   kc_options o;
@@ -986,6 +1008,7 @@ __global__ void mismatch_gather_kernel(const uint32_t* ids, uint32_t m, const ui
 }
 
 kc_status kc_peel(kc_graph* g, uint32_t* coreness, kc_stats* st) {
+  kcb::DeviceGuard device_guard;  // restore the caller's current device
   g_last_error.clear();
   if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
   if (g->n && !coreness) return fail(KC_ERR_INVALID_ARGUMENT, "coreness is null");
@@ -1032,6 +1055,7 @@ __global__ void tail_out_kernel(const uint32_t* E, const uint32_t* perm, uint32_
 
 kc_status kc_sequential_tail(kc_graph* g, uint32_t* est, uint8_t* active, int extended_notify,
                              kc_stats* st) {
+  kcb::DeviceGuard device_guard;  // restore the caller's current device
   g_last_error.clear();
   if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
   if (g->n && (!est || !active)) return fail(KC_ERR_INVALID_ARGUMENT, "est / active is null");
@@ -1104,6 +1128,7 @@ kc_status kc_sequential_tail(kc_graph* g, uint32_t* est, uint8_t* active, int ex
 
 kc_status kc_verify(kc_graph* g, const kc_options* opt, kc_mismatch* out, uint64_t cap,
                     uint64_t* count) {
+  kcb::DeviceGuard device_guard;  // restore the caller's current device
   g_last_error.clear();
   if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null graph");
   if (!count) return fail(KC_ERR_INVALID_ARGUMENT, "count is null");

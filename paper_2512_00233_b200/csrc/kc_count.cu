@@ -307,6 +307,8 @@ __device__ __noinline__ void wq_flush(const CP<OffT, EstT>& p, const Enq& q, int
   uint32_t base = 0;
   if (lane_id() == 0) base = atomicAdd(&q.qn[c], n);
   base = __shfl_sync(FULL, base, 0);
+  KC_BOUNDS(p.cb[c] + base + n <= p.cb[c + 1]);  // a class never holds more than its ids
+  KC_BOUNDS(n <= (uint32_t)WQ);
   for (uint32_t i = lane_id(); i < n; i += 32) q.qnext[p.cb[c] + base + i] = q.wbuf[c * WQ + i];
   __syncwarp();
   if (lane_id() == 0) q.wn[c] = 0;
@@ -327,6 +329,7 @@ __device__ __noinline__ void wq_flush_all(const CP<OffT, EstT>& p, const Enq& q)
     const uint32_t nc = __shfl_sync(FULL, n, c);
     if (!nc) continue;
     const uint32_t bc = __shfl_sync(FULL, base, c);
+    KC_BOUNDS(nc <= (uint32_t)WQ && p.cb[c] + bc + nc <= p.cb[c + 1]);
     for (uint32_t i = lane; i < nc; i += 32) q.qnext[p.cb[c] + bc + i] = q.wbuf[c * WQ + i];
   }
   __syncwarp();
@@ -343,6 +346,8 @@ __device__ __noinline__ void wq_push(const CP<OffT, EstT>& p, const Enq& q, bool
     const uint32_t m = __ballot_sync(FULL, c == cc);
     if (!m) continue;
     const uint32_t n0 = q.wn[cc];
+    KC_BOUNDS(n0 + __popc(m) <= (uint32_t)WQ);
+    KC_BOUNDS(c != cc || id < p.n_nz);
     if (c == cc) q.wbuf[cc * WQ + n0 + __popc(m & lanemask_lt())] = id;
     __syncwarp();
     if (lane_id() == 0) q.wn[cc] = n0 + __popc(m);
@@ -417,7 +422,10 @@ __device__ __forceinline__ uint2 warp_window(const uint32_t* src, bool ro, const
                          for (int k = 0; k < 8; ++k) {
                            if (!(ok >> k & 1)) continue;
                            if (x[k] >= top) ++above;
-                           else if (x[k] >= L) atomicAdd(&bins[(top - 1 - x[k]) / w], 1u);
+                           else if (x[k] >= L) {
+                             KC_BOUNDS((top - 1 - x[k]) / w < (uint32_t)WARP_BINS);
+                             atomicAdd(&bins[(top - 1 - x[k]) / w], 1u);
+                           }
                          }
                        }, KC_CUT_EVAL && (KC_CUT_LISTS || ro) ? dc.at(L) : 0xffffffffu, KC_CUT_EVAL && ro && dc.sorted);
     __syncwarp();
@@ -469,7 +477,10 @@ __device__ __noinline__ void cta_window(const uint32_t* src, bool ro, const EstT
                                     for (int k = 0; k < 8; ++k) {
                                       if (!(ok >> k & 1)) continue;
                                       if (x[k] >= top) ++above;
-                                      else if (x[k] >= L) atomicAdd(&s_hist[(top - 1 - x[k]) / w], 1u);
+                                      else if (x[k] >= L) {
+                                        KC_BOUNDS((top - 1 - x[k]) / w < (uint32_t)HIST_BINS);
+                                        atomicAdd(&s_hist[(top - 1 - x[k]) / w], 1u);
+                                      }
                                     }
                                   }, KC_CUT_EVAL && (KC_CUT_LISTS || ro) ? dc.at(L) : 0xffffffffu, KC_CUT_EVAL && ro && dc.sorted);
     const uint32_t C = block_sum(above, s_red);
@@ -618,6 +629,7 @@ __device__ __forceinline__ void finish_eval(const CP<OffT, EstT>& p, const View<
     }
     return;
   }
+  KC_BOUNDS(it.u < p.n_nz);
   acc.evals += 1;
   acc.escan += it.deg;
   acc.ascan += scanned;
@@ -740,6 +752,7 @@ __device__ void huge_warps(const CP<OffT, EstT>& p, const View<EstT>& v, Shared&
     if (!warp_fn(u)) {  // too long for a warp: to the CTA-wide queue
       if (lane_id() == 0) {
         const uint32_t slot = atomicAdd(&ctl.lqn[ph], 1u);
+        KC_BOUNDS(slot < p.cb[1] + 1);
         atomicExch(&p.lq[ph][slot], u);
       }
     }
@@ -937,7 +950,10 @@ __device__ __forceinline__ void flat_eval_impl(const CP<OffT, EstT>& p, const Vi
                     if (!(ok >> j & 1)) continue;
                     const uint32_t sj = seg[j];
                     const uint32_t cp = fw.hi[sj];
-                    if (x[j] < cp && x[j] >= fw.lo[sj]) atomicAdd(&bins[sj * fb + (cp - 1 - x[j])], 1u);
+                    if (x[j] < cp && x[j] >= fw.lo[sj]) {
+                      KC_BOUNDS(sj < 32 && cp - 1 - x[j] < fb && sj * fb + (cp - 1 - x[j]) < (uint32_t)WARP_BINS);
+                      atomicAdd(&bins[sj * fb + (cp - 1 - x[j])], 1u);
+                    }
                   }
                 });
     __syncwarp();
@@ -1250,7 +1266,10 @@ __device__ __forceinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const E
                          for (int k = 0; k < 8; ++k) {
                            if (!(ok >> k & 1)) continue;
                            if (x[k] >= t) ++above;
-                           else if (x[k] >= slo) atomicAdd(&bins[t - 1 - x[k]], 1u);
+                           else if (x[k] >= slo) {
+                             KC_BOUNDS(t - 1 - x[k] < (uint32_t)KC_SPEC_BINS);
+                             atomicAdd(&bins[t - 1 - x[k]], 1u);
+                           }
                          }
                        }
                        if (build) {
@@ -1262,7 +1281,10 @@ __device__ __forceinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const E
                          uint32_t pos = cursor + incl - nk;
 #pragma unroll
                          for (int k = 0; k < 8; ++k)
-                           if (keep >> k & 1) p.radj[ob + pos++] = ids[k];
+                           if (keep >> k & 1) {
+                             KC_BOUNDS(pos < len);  // a list is a subset of its row
+                             p.radj[ob + pos++] = ids[k];
+                           }
                          cursor += __shfl_sync(FULL, incl, 31);
                        }
                      }, CUT ? p.dc.at(need) : 0xffffffffu, CUT && ro && p.dc.sorted);
@@ -1320,7 +1342,10 @@ __device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p, const Enq& 
                                     for (int k = 0; k < 8; ++k) {
                                       if (!(ok >> k & 1)) continue;
                                       if (x[k] >= t) ++above;
-                                      else if (x[k] >= slo) atomicAdd(&s_hist[t - 1 - x[k]], 1u);
+                                      else if (x[k] >= slo) {
+                                        KC_BOUNDS(t - 1 - x[k] < (uint32_t)HIST_BINS);
+                                        atomicAdd(&s_hist[t - 1 - x[k]], 1u);
+                                      }
                                     }
                                   }
                                   if (build) {
@@ -1336,7 +1361,10 @@ __device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p, const Enq& 
                                     uint32_t pos = __shfl_sync(FULL, base, 0) + incl - nk;
 #pragma unroll
                                     for (int k = 0; k < 8; ++k)
-                                      if (keep >> k & 1) p.radj[ob + pos++] = ids[k];
+                                      if (keep >> k & 1) {
+                                        KC_BOUNDS(pos < len);
+                                        p.radj[ob + pos++] = ids[k];
+                                      }
                                   }
                                 }, KC_CUT_NOTIFY && (KC_CUT_LISTS || ro) ? p.dc.at(need) : 0xffffffffu, KC_CUT_NOTIFY && ro && p.dc.sorted);
   if (tag) {  // CTA suffix scan of the spec window (one pass, no refinement)
@@ -1538,7 +1566,10 @@ __device__ __forceinline__ void flat_notify_impl(const CP<OffT, EstT>& p, const 
                       cc = 0;
                     }
                     if (v && x[j] >= tj) ++cc;
-                    else if (v && x[j] >= fw.slo[sj]) atomicAdd(&bins[sj * FB + (tj - 1 - x[j])], 1u);
+                    else if (v && x[j] >= fw.slo[sj]) {
+                      KC_BOUNDS(tj - 1 - x[j] < FB && sj * FB + (tj - 1 - x[j]) < (uint32_t)WARP_BINS);
+                      atomicAdd(&bins[sj * FB + (tj - 1 - x[j])], 1u);
+                    }
                   }
                   if (cc) atomicAdd(&fw.above[cs], cc);
                   uint32_t act = 0;
@@ -1780,6 +1811,7 @@ __device__ __forceinline__ void eval_phase(const CP<OffT, EstT>& p, const View<E
   });
   consume_long(p, v, sh, ctl, ph, false, eval_long);
   if (pf) pf[2] = gtimer();
+  KC_BOUNDS(blockDim.x == SOLVE_THREADS);
   if (v.r0 || PULL || !KC_FLAT_EVAL) {
     eval_wclass<PULL>(p, v, s_cache, w_bins, C_BIG, GMAX_BIG, acc);
     eval_wclass<PULL>(p, v, s_cache, w_bins, C_WARP, GMAX_WARP, acc);
@@ -1844,6 +1876,7 @@ __device__ __noinline__ void compact_pull(const CP<OffT, EstT>& p, uint32_t* qcn
         for (int j = 0; j < 16; ++j)
           if (m >> j & 1) {
             const uint32_t u = a + j;
+            KC_BOUNDS(pos < b1);
             queue[pos++] = u;
             p.pflag[u] = 0;
             p.N[u] = (EstT)p.spec_t[u];

@@ -7,6 +7,7 @@
 // the answer is the largest level t >= 1 with count(>= t) >= t.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 
 #include "kc_internal.h"
 
@@ -14,6 +15,29 @@ namespace kcb {
 namespace dev {
 
 constexpr unsigned FULL = 0xffffffffu;
+
+// KC_DEBUG_BOUNDS=1 (scripts/build_debug_bounds.sh): every queue, list,
+// long-scan-queue, histogram and per-vertex index the solvers write is
+// checked; a violation prints its site and traps (the launch fails with a
+// CUDA error, the C-ABI returns KC_ERR_CUDA).  compute-sanitizer is closed on
+// this pool, so this build stands in for its bounds checks.
+#ifndef KC_DEBUG_BOUNDS
+#define KC_DEBUG_BOUNDS 0
+#endif
+#if KC_DEBUG_BOUNDS
+#define KC_BOUNDS(cond)                                                                  \
+  do {                                                                                   \
+    if (!(cond)) {                                                                       \
+      printf("KC_BOUNDS %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, \
+             threadIdx.x, #cond);                                                        \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define KC_BOUNDS(cond) \
+  do {                  \
+  } while (0)
+#endif
 constexpr uint32_t NWARPS = SOLVE_THREADS / 32;
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
@@ -201,7 +225,10 @@ template <int NB>
 __device__ __forceinline__ void tally(uint32_t x, uint32_t top, uint32_t floor, uint32_t& above,
                                       uint32_t* bins) {
   if (x >= top) ++above;
-  else if ((int)x >= (int)top - NB && x >= floor) atomicAdd(&bins[top - 1 - x], 1u);
+  else if ((int)x >= (int)top - NB && x >= floor) {
+    KC_BOUNDS(top - 1 - x < (uint32_t)NB);
+    atomicAdd(&bins[top - 1 - x], 1u);
+  }
 }
 
 // Suffix scan of one window (kernel.hpp:36-41): the smallest bin i whose

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/kcore_b200.h"
+#include "kc_internal.h"
 
 namespace {
 
@@ -384,6 +385,7 @@ extern "C" {
 
 kc_status kc_gen_config(int cfg, uint64_t p0, uint64_t p1, uint64_t p2, uint64_t seed, int device,
                         kc_csr_dev** out) {
+  kcb::DeviceGuard device_guard;  // restore the caller's current device
   if (!out) return KC_ERR_INVALID_ARGUMENT;
   *out = nullptr;
   int count = 0;
@@ -469,6 +471,7 @@ kc_status kc_gen_config(int cfg, uint64_t p0, uint64_t p1, uint64_t p2, uint64_t
 }
 
 void kc_csr_dev_free(kc_csr_dev* g) {
+  kcb::DeviceGuard device_guard;  // restore the caller's current device
   if (!g) return;
   cudaSetDevice(g->device);
   cudaFree(const_cast<uint64_t*>(g->view.offsets));
@@ -478,6 +481,7 @@ void kc_csr_dev_free(kc_csr_dev* g) {
 }
 
 kc_status kc_csr_dev_download(const kc_csr_dev* g, uint64_t* offsets, uint32_t* neighbors) {
+  kcb::DeviceGuard device_guard;  // restore the caller's current device
   if (!g || !offsets) return KC_ERR_INVALID_ARGUMENT;
   GK(cudaSetDevice(g->device));
   GK(cudaMemcpy(offsets, g->view.offsets, ((size_t)g->view.n + 1) * 8, cudaMemcpyDeviceToHost));

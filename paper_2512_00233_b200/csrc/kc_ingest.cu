@@ -175,6 +175,7 @@ void describe(const char* text, uint64_t len, uint64_t b, uint64_t e, uint64_t k
 
 kc_status ingest(const char* host_text, uint64_t len, int device, kc_csr_dev** out,
                  kc_parse_error* err) {
+  kcb::DeviceGuard device_guard;  // restore the caller's current device
   *out = nullptr;
   if (err) {
     err->line = 0;
@@ -351,6 +352,7 @@ kc_status kc_load_edge_list_file(const char* path, int device, kc_csr_dev** out,
 }
 
 kc_status kc_csr_dev_original_ids(const kc_csr_dev* g, uint64_t* ids) {
+  kcb::DeviceGuard device_guard;  // restore the caller's current device
   if (!g || (g->view.n && !ids)) return KC_ERR_INVALID_ARGUMENT;
   if (!g->view.n) return KC_OK;
   if (cudaSetDevice(g->device) != cudaSuccess) return KC_ERR_CUDA;

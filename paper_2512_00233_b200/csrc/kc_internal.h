@@ -125,9 +125,28 @@ cudaError_t launch_init(const SolveBuffers& b, bool est16, bool off64, uint32_t 
 // Max shared memory the solver may use for the estimate cache (bytes).
 size_t solver_cache_bytes_max();
 
-// Stream-ordered device allocation from the device's default memory pool,
-// kept (release threshold = max) so repeated upload / solve / free cycles do
-// not pay cudaMalloc / cudaFree (kc_api.cu).
+// The caller's current device is restored when a C-ABI entry point returns
+// (every entry point that selects the graph's device holds one).
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      prev = -1;
+      cudaGetLastError();
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// Stream-ordered device allocation from the library's own memory pool (one
+// per device, created on first use), kept (release threshold = max) so
+// repeated upload / solve / free cycles do not pay cudaMalloc / cudaFree —
+// without changing the device's default pool, which co-resident libraries
+// (PyTorch, CuPy) may use (kc_api.cu).
 cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t s);
 void dfree(void* p, cudaStream_t s);
 template <typename T>
@@ -168,6 +187,8 @@ struct PrepOut {
   uint32_t max_degree;
   uint32_t cls_begin[NCLS + 1];
   bool off64;
+  bool invalid;     // the input is not a CSR (offsets not 0..nnz non-decreasing, or a
+                    // neighbour id >= n): nothing was laid out
 };
 // Pipelined upload (host CSR): the neighbours arrive in k chunks of old row
 // ids [old_lo[c], old_lo[c+1]) (host array, k + 1 entries), chunk c complete

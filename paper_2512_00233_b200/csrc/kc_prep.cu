@@ -24,10 +24,19 @@
 namespace kcb {
 namespace {
 
-__global__ void degrees_kernel(const uint64_t* __restrict__ off, uint32_t n,
-                               uint32_t* __restrict__ deg, uint32_t* __restrict__ iota) {
+// Degrees, and the CSR's structural checks the reference's Graph guarantees
+// by construction (graph.hpp:37-75): offsets[0] == 0, non-decreasing,
+// offsets[n] == nnz, every degree < 2^32.  A violation sets *bad (the
+// upload then fails with KC_ERR_INVALID_ARGUMENT instead of indexing out of
+// bounds in the layout or the solver).
+__global__ void degrees_kernel(const uint64_t* __restrict__ off, uint32_t n, uint64_t nnz,
+                               uint32_t* __restrict__ deg, uint32_t* __restrict__ iota,
+                               uint32_t* bad) {
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
-    deg[u] = (uint32_t)(off[u + 1] - off[u]);
+    const uint64_t a = off[u], b = off[u + 1];
+    if (b < a || b - a > 0xffffffffull || (u == 0 && a != 0) || (u == n - 1 && b != nnz))
+      atomicOr(bad, 1u);
+    deg[u] = b >= a ? (uint32_t)(b - a) : 0u;
     iota[u] = u;
   }
 }
@@ -100,7 +109,7 @@ __global__ void relabel_rows_kernel(const uint64_t* __restrict__ old_off,
                                     const uint64_t* __restrict__ chunk_base,  // per row, scan of chunks
                                     uint32_t n_nz, const OffT* __restrict__ new_off,
                                     uint32_t* __restrict__ new_adj, uint64_t total_chunks,
-                                    uint32_t o_lo, uint32_t o_hi) {
+                                    uint32_t o_lo, uint32_t o_hi, uint32_t n, uint32_t* bad) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
@@ -119,7 +128,11 @@ __global__ void relabel_rows_kernel(const uint64_t* __restrict__ old_off,
     const uint64_t k1 = k0 + 1024 < deg ? k0 + 1024 : deg;
     const uint32_t* src = old_adj + old_off[o];
     uint32_t* dst = new_adj + new_off[i];
-    for (uint64_t k = k0 + lane; k < k1; k += 32) dst[k] = inv[src[k]];
+    for (uint64_t k = k0 + lane; k < k1; k += 32) {
+      const uint32_t x = src[k];
+      if (x >= n) atomicOr(bad, 2u);  // neighbour id out of range
+      dst[k] = x < n ? inv[x] : 0u;
+    }
   }
 }
 
@@ -132,7 +145,7 @@ __global__ void relabel_small_rows_kernel(const uint64_t* __restrict__ old_off,
                                           const uint32_t* __restrict__ inv, uint32_t first,
                                           uint32_t n_nz, const OffT* __restrict__ new_off,
                                           uint32_t* __restrict__ new_adj, uint32_t o_lo,
-                                          uint32_t o_hi) {
+                                          uint32_t o_hi, uint32_t n, uint32_t* bad) {
   const uint32_t k = threadIdx.x & 7;
   const uint64_t t0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 3;
   const uint64_t nt = (gridDim.x * (uint64_t)blockDim.x) >> 3;
@@ -151,7 +164,10 @@ __global__ void relabel_small_rows_kernel(const uint64_t* __restrict__ old_off,
 #pragma unroll
     for (int j = 0; j < (int)(DEG_SUB_MAX / 8); ++j) {
       const uint32_t e = k + 8u * j;
-      if (e < deg) new_adj[b + e] = inv[v[j]];
+      if (e < deg) {
+        if (v[j] >= n) atomicOr(bad, 2u);  // neighbour id out of range
+        new_adj[b + e] = v[j] < n ? inv[v[j]] : 0u;
+      }
     }
   }
 }
@@ -194,7 +210,8 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
   uint32_t* sort_tmp = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0, need = 0;
-  uint32_t hb[7] = {0, 0, 0, 0, 0, 0, 0};
+  uint32_t hb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  out->invalid = false;
   const bool off64 = force_off64 || nnz >= (1ull << 32);
   const int G = 148 * 8, B = 256;
   out->off = nullptr;
@@ -210,7 +227,8 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
   PREP_CK(dalloc(&perm, n, s));
   PREP_CK(dalloc(&inv, n, s));
   PREP_CK(dalloc(&bounds, 8, s));
-  degrees_kernel<<<G, B, 0, s>>>(off, n, deg, iota);
+  PREP_CK(cudaMemsetAsync(bounds, 0, 8 * sizeof(uint32_t), s));
+  degrees_kernel<<<G, B, 0, s>>>(off, n, nnz, deg, iota, bounds + 7);
   PREP_CK(cudaGetLastError());
   // stable descending radix sort of (degree, id)
   PREP_CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, need, deg, sdeg, iota, perm, n, 0, 32, s));
@@ -223,6 +241,10 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
   PREP_CK(cudaGetLastError());
   PREP_CK(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, s));
   PREP_CK(cudaStreamSynchronize(s));
+  if (hb[7]) {  // malformed offsets: nothing below may trust them
+    out->invalid = true;
+    goto done;
+  }
   out->h_graph = hb[0];
   out->max_degree = hb[6];
   out->n_nz = hb[5];
@@ -295,22 +317,22 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
         if (off64)
           relabel_small_rows_kernel<uint64_t><<<G, B, 0, s>>>(off, adj, perm, inv, n_big, n_nz,
                                                               (const uint64_t*)new_off, new_adj,
-                                                              o_lo, o_hi);
+                                                              o_lo, o_hi, n, bounds + 7);
         else
           relabel_small_rows_kernel<uint32_t><<<G, B, 0, s>>>(off, adj, perm, inv, n_big, n_nz,
                                                               (const uint32_t*)new_off, new_adj,
-                                                              o_lo, o_hi);
+                                                              o_lo, o_hi, n, bounds + 7);
         PREP_CK(cudaGetLastError());
       }
       if (n_big) {
         if (off64)
           relabel_rows_kernel<uint64_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_big,
                                                         (const uint64_t*)new_off, new_adj, total,
-                                                        o_lo, o_hi);
+                                                        o_lo, o_hi, n, bounds + 7);
         else
           relabel_rows_kernel<uint32_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_big,
                                                         (const uint32_t*)new_off, new_adj, total,
-                                                        o_lo, o_hi);
+                                                        o_lo, o_hi, n, bounds + 7);
         PREP_CK(cudaGetLastError());
       }
     }
@@ -353,6 +375,11 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
       PREP_CK(cudaGetLastError());
     }
     PREP_CK(cudaStreamSynchronize(s));
+    PREP_CK(cudaMemcpy(hb + 7, bounds + 7, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    if (hb[7]) {  // a neighbour id >= n
+      out->invalid = true;
+      goto done;
+    }
   }
   out->off = new_off;
   out->adj = new_adj;

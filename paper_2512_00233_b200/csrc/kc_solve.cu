@@ -206,6 +206,7 @@ __device__ void compact_frontier(const P<OffT, EstT>& p, uint8_t* flags, uint32_
 #pragma unroll
         for (int j = 0; j < 16; ++j)
           if (m >> j & 1) {
+            KC_BOUNDS(pos < b1);
             p.queue[pos++] = a + j;
             flags[a + j] = 0;
           }

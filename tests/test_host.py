@@ -52,3 +52,17 @@ def test_named_graph_fixtures_roundtrip():
         G = K.Graph.from_edges(g["n"], g["edges"])
         assert G.offsets().tolist() == g["offsets"], name
         assert G.neighbor_array().tolist() == g["neighbors"], name
+
+
+def test_graph_rejects_malformed_csr():
+    """The reference's Graph cannot be built in an invalid state
+    (graph.hpp:37-75): the Python mirror rejects what the device would
+    otherwise index out of bounds with."""
+    import pytest
+    import paper_2512_00233_b200 as K
+    with pytest.raises(ValueError):
+        K.Graph(np.array([0, 2, 1, 3], np.uint64), np.array([1, 2, 0], np.uint32))  # decreasing
+    with pytest.raises(ValueError):
+        K.Graph(np.array([0, 1, 2], np.uint64), np.array([1, 5], np.uint32))  # id >= n
+    with pytest.raises(ValueError):
+        K.Graph(np.array([1, 2], np.uint64), np.array([0], np.uint32))  # offsets[0] != 0
