@@ -12,12 +12,17 @@ independent replicas (the path does not shard in this tier: "replicas only").
 value   = ref-equivalent GTEPS = E_scan of the reference rule (fastk.cpp
           notify on settled values, computed by the same solver in REFERENCE
           mode, untimed) / device time to converged coreness, inputs resident
-          in HBM; summed over replicas.
-e2e     = the same metric through the public C-ABI call with HOST buffers:
-          pinned CSR -> kc_graph_upload (H2D + layout) -> kc_solve -> coreness
-          on the host, per step.
+          in HBM; summed over replicas.  It is a time ratio against the
+          reference arm (which reports the same E_scan over its own time);
+          the solver's own GTEPS is config.gteps_own_rule.
+e2e     = the same metric through the public C-ABI one-shot call
+          kc_fastk_run with HOST buffers (H2D + layout + solve + D2H every
+          step): pinned buffers (e2e) and the pageable arrays a reference
+          Graph holds (e2e.pageable).
 roofline= algorithmic bytes (8 * E_scan + 16 * V_eval of the run)
           / solver-kernel time vs MEASURED_PEAKS.json hbm_gbs.
+also    = the second north-star graph (--also, default cfg5 = R-MAT scale
+          26) measured in the same run, inside the same JSON line.
 """
 from __future__ import annotations
 
@@ -171,19 +176,14 @@ def profile_traffic(cfg: int, kernel: str):
         return None
 
 
-def run_ours(args, ws, rank, local):
-    import torch
-    import paper_2512_00233_b200 as K
-
-    torch.cuda.set_device(local)
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    desc, (p0, p1, p2), seed = CONFIGS[args.config]
-    if args.scale:
+def measure(K, torch, cfg, args, local, steps, warmup, e2e_steps, dist=None, ws=1):
+    """One workload: device-resident solves (CUDA events on the library's
+    stream, L2 flushed before each), then the reference-facing one-shot call
+    kc_fastk_run with host buffers (pinned, then pageable)."""
+    desc, (p0, p1, p2), seed = CONFIGS[cfg]
+    if args.scale and cfg == args.config:
         p0 = args.scale
-    dcsr = K.gen_config(args.config, p0, p1, p2, seed=seed + args.seed_offset, device=local)
+    dcsr = K.gen_config(cfg, p0, p1, p2, seed=seed + args.seed_offset, device=local)
     n, nnz = dcsr.n, dcsr.nnz
     gg = K.GpuGraph(dcsr, device=local)
     t_upload, t_prep = gg.timings()
@@ -199,7 +199,7 @@ def run_ours(args, ws, rank, local):
         torch.cuda.synchronize()
         return gg.solve_device(out.data_ptr(), opts)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     if dist:
         dist.barrier()
@@ -207,73 +207,148 @@ def run_ours(args, ws, rank, local):
     stats = []
     with Clocks(local) as clk:
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(steps):
             stats.append(step())
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
     if dist:
         dist.barrier()
-    ms = [s["t_solve_ms"] for s in stats]
+    ms = [x["t_solve_ms"] for x in stats]
     ms_step = reduce_max(sum(ms) / len(ms), dist, device=f"cuda:{local}")
     st = stats[-1]
-    e_ref, e_our, v_our = st_ref["e_scan"], st["e_scan"], st["v_eval"]
-    gteps = ws * e_ref / (ms_step * 1e-3) / 1e9
+    launches = sum(int(x["kernel_launches"]) for x in stats)
+    gg.free()
+    del flush
+    torch.cuda.synchronize()
 
-    # e2e through the public C-ABI with pinned host buffers (rank-local)
+    # e2e through the public C-ABI one-shot call (fastk_run semantics): host
+    # CSR in, coreness out, every step.  Pinned host buffers, then the
+    # pageable arrays a reference Graph holds (graph.hpp:72-73).
     host = dcsr.download()
+    dcsr.free()
     off_p = torch.from_numpy(host.offsets().view(np.int64)).pin_memory()
     nbr_p = torch.from_numpy(host.neighbor_array().view(np.int32)).pin_memory()
     pinned = K.Graph(off_p.numpy().view(np.uint64), nbr_p.numpy().view(np.uint32))
     core_p = torch.empty(max(n, 1), dtype=torch.int32).pin_memory()
     core_np = core_p.numpy().view(np.uint32)
-    e2e_steps = max(1, min(args.steps, 5))
-    e2e_ms, parts = [], []
-    for i in range(e2e_steps + 1):
-        t = time.perf_counter()
-        # kc_fastk_run: the reference-facing one-shot call (fastk_run semantics)
-        _, st2 = K.fastk_run_abi(pinned, opts, out=core_np)
-        if i:  # first call warms up
-            e2e_ms.append((time.perf_counter() - t) * 1e3)
-            parts.append({k: st2[k] for k in ("t_upload_ms", "t_prep_ms", "t_solve_ms",
-                                              "t_download_ms")})
-    e2e_ms_step = reduce_max(sum(e2e_ms) / len(e2e_ms), dist, device=f"cuda:{local}")
 
+    def e2e(graph, out_arr, k):
+        times, parts = [], []
+        for i in range(k + 1):
+            t = time.perf_counter()
+            _, st2 = K.fastk_run_abi(graph, opts, out=out_arr)
+            if i:  # the first call warms up
+                times.append((time.perf_counter() - t) * 1e3)
+                parts.append({kk: st2[kk] for kk in ("t_upload_ms", "t_prep_ms", "t_solve_ms",
+                                                     "t_download_ms")})
+        return (reduce_max(sum(times) / len(times), dist, device=f"cuda:{local}"),
+                {kk: round(statistics.mean(p[kk] for p in parts), 3) for kk in parts[0]})
+
+    e2e_ms, e2e_parts = e2e(pinned, core_np, e2e_steps)
+    pinned_ok = bool(off_p.is_pinned() and nbr_p.is_pinned())
+    del pinned, off_p, nbr_p, core_p, core_np
+    core_pg = np.zeros(max(n, 1), dtype=np.uint32)
+    e2e_pg_ms, e2e_pg_parts = e2e(host, core_pg, max(1, min(e2e_steps, 5)))
+    return dict(cfg=cfg, desc=desc, n=n, nnz=nnz, host=host, st=st, st_ref=st_ref,
+                ms_step=ms_step, wall=wall, clk=clk.summary(), launches=launches,
+                t_upload=t_upload, t_prep=t_prep, e2e_ms=e2e_ms, e2e_parts=e2e_parts,
+                e2e_pg_ms=e2e_pg_ms, e2e_pg_parts=e2e_pg_parts, pinned=pinned_ok,
+                e2e_steps=e2e_steps, ws=ws)
+
+
+def roofline(m, rule):
     peak, peak_src = measured_peak()
-    bytes_alg = 8 * e_our + 16 * v_our
-    achieved = bytes_alg / (ms_step * 1e-3) / 1e9
-    kname = solver_kernel(args.rule)
-    traffic = profile_traffic(args.config, kname)
+    st = m["st"]
+    bytes_alg = 8 * st["e_scan"] + 16 * st["v_eval"]
+    achieved = bytes_alg / (m["ms_step"] * 1e-3) / 1e9
+    kname = solver_kernel(rule)
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": profile_traffic(m["cfg"], kname),
+            "peak_source": peak_src, "kernel": f"{kname} (persistent)",
+            "bytes_alg_per_launch": bytes_alg}
+
+
+def e2e_obj(m):
+    n, nnz, ws = m["n"], m["nnz"], m["ws"]
+    e_ref = m["st_ref"]["e_scan"]
+    return {"value": round(ws * e_ref / (m["e2e_ms"] * 1e-3) / 1e9, 3), "unit": UNIT,
+            "ms_per_step": round(m["e2e_ms"], 3), "steps": m["e2e_steps"],
+            "h2d_bytes_per_step": int((n + 1) * 8 + nnz * 4),
+            "d2h_bytes_per_step": int(n * 4),
+            "device_ms": m["e2e_parts"],
+            "call": "kc_fastk_run (pinned host CSR in, coreness to pinned host memory)",
+            "pinned": m["pinned"],
+            "pageable": {"value": round(ws * e_ref / (m["e2e_pg_ms"] * 1e-3) / 1e9, 3),
+                         "ms_per_step": round(m["e2e_pg_ms"], 3), "device_ms": m["e2e_pg_parts"],
+                         "call": "kc_fastk_run on pageable numpy arrays (a reference Graph's "
+                                 "std::vector storage, graph.hpp:72-73)"}}
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_2512_00233_b200 as K
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    m = measure(K, torch, args.config, args, local, args.steps, args.warmup,
+                max(1, args.steps), dist, ws)
+    st, e_ref = m["st"], m["st_ref"]["e_scan"]
+    ms_step = m["ms_step"]
     line = {
-        "metric": METRIC, "value": round(gteps, 3), "unit": UNIT, "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16" if st["h_graph"] < 32768 else "u32",
+        "metric": METRIC, "value": round(ws * e_ref / (ms_step * 1e-3) / 1e9, 3), "unit": UNIT,
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u16" if st["h_graph"] < 32768 else "u32",
         "data": "synthetic (kcgen v1 seeded generator, built in HBM)",
-        "config": {"workload": f"cfg{args.config}: {desc}", "n": n, "nnz": nnz,
+        "config": {"workload": f"cfg{args.config}: {m['desc']}", "n": m["n"], "nnz": m["nnz"],
                    "parallelism": f"replicas{ws}" if ws > 1 else "single GPU",
                    "rule": K.Rule(args.rule).name.lower(),
                    "l2": "flushed (256 MiB write) before every step; CSR > L2",
                    "ms_to_converged": round(ms_step, 4),
-                   "e_scan_ref": e_ref, "e_scan": e_our, "v_eval": v_our,
+                   "value_is": "ref-equivalent GTEPS = the reference rule's E_scan (same graph, "
+                               "untimed REFERENCE-rule solve) / this run's time to converged "
+                               "coreness, summed over replicas: a time ratio against the "
+                               "reference arm, whose value is the same E_scan / its time",
+                   "e_scan_ref": e_ref, "e_scan": st["e_scan"], "v_eval": st["v_eval"],
                    "iterations": st["iterations"], "k_max": st["k_max"],
-                   "h_graph": st["h_graph"], "gteps_own_rule": round(e_our / ms_step / 1e6, 3),
-                   "t_upload_ms": round(t_upload, 3), "t_prep_ms": round(t_prep, 3),
-                   "wall_s_timed_region": round(wall, 4)},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "peak_source": peak_src, "kernel": f"{kname} (persistent)",
-                     "bytes_alg_per_launch": bytes_alg},
-        "e2e": {"value": round(ws * e_ref / (e2e_ms_step * 1e-3) / 1e9, 3), "unit": UNIT,
-                "ms_per_step": round(e2e_ms_step, 3),
-                "h2d_bytes_per_step": int((n + 1) * 8 + nnz * 4),
-                "device_ms": {k: round(statistics.mean(p[k] for p in parts), 3) for k in parts[0]},
-                "call": "kc_fastk_run (pinned host CSR in, coreness to pinned host memory)",
-                "pinned": bool(off_p.is_pinned() and nbr_p.is_pinned()),
-                "d2h_bytes_per_step": int(n * 4)},
-        "gpu_launches": 4 * args.steps,
-        "clocks": clk.summary(),
+                   "h_graph": st["h_graph"],
+                   "gteps_own_rule": round(st["e_scan"] / ms_step / 1e6, 3),
+                   "t_upload_ms": round(m["t_upload"], 3), "t_prep_ms": round(m["t_prep"], 3),
+                   "wall_s_timed_region": round(m["wall"], 4)},
+        "roofline": roofline(m, args.rule),
+        "e2e": e2e_obj(m),
+        "gpu_launches": m["launches"],
+        "clocks": m["clk"],
     }
+    host = m.pop("host")
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(host, args)
+    del host, m
+    # the second north-star graph (R-MAT scale 26), measured in the same run
+    # and reported inside the same JSON line (rank 0 prints one line)
+    if ws == 1 and args.also:
+        also = {}
+        for c in [int(x) for x in args.also.split(",") if x]:
+            if c == args.config:
+                continue
+            torch.cuda.empty_cache()
+            a = measure(K, torch, c, args, local, 5, 3, 3)
+            a.pop("host")
+            sta = a["st"]
+            also[f"cfg{c}"] = {
+                "workload": f"cfg{c}: {a['desc']}", "n": a["n"], "nnz": a["nnz"],
+                "value": round(a["st_ref"]["e_scan"] / (a["ms_step"] * 1e-3) / 1e9, 3),
+                "unit": UNIT, "ms_to_converged": round(a["ms_step"], 4), "steps": 5,
+                "e_scan_ref": a["st_ref"]["e_scan"], "e_scan": sta["e_scan"],
+                "v_eval": sta["v_eval"], "iterations": sta["iterations"], "k_max": sta["k_max"],
+                "t_prep_ms": round(a["t_prep"], 3),
+                "roofline": roofline(a, args.rule), "e2e": e2e_obj(a),
+                "gpu_launches": a["launches"], "clocks": a["clk"]}
+            line["gpu_launches"] += a["launches"]
+        line["also"] = also
     if dist:
         dist.destroy_process_group()
     if rank == 0:
@@ -367,6 +442,9 @@ def main():
     ap.add_argument("--rule", type=int, default=2, help="0 reference, 1 counting, 2 auto (= counting)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--also", default="5",
+                    help="further configs measured in the same run (N=1), reported under "
+                         "'also' in the same JSON line ('' to skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_env()

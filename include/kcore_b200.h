@@ -94,7 +94,8 @@ typedef struct kc_stats {
   float t_prep_ms;           /* on-device relabel / layout (kc_graph_upload) */
   float t_solve_ms;          /* init -> converged estimates, CSR resident */
   float t_download_ms;       /* permute-back + D2H of the coreness */
-  uint32_t reserved[8];
+  uint32_t kernel_launches;  /* this library's kernels launched by the call (solve path) */
+  uint32_t reserved[7];
 } kc_stats;
 
 /* A borrowed view of an undirected simple CSR: offsets has n+1 entries,

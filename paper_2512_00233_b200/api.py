@@ -38,7 +38,7 @@ class _Stats(C.Structure):
                 ("tail_rounds", C.c_uint64), ("k_max", C.c_uint32), ("h_graph", C.c_uint32),
                 ("k_avg", C.c_double), ("t_upload_ms", C.c_float), ("t_prep_ms", C.c_float),
                 ("t_solve_ms", C.c_float), ("t_download_ms", C.c_float),
-                ("reserved", C.c_uint32 * 8)]
+                ("kernel_launches", C.c_uint32), ("reserved", C.c_uint32 * 7)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}

@@ -20,7 +20,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libkcore_b200.so")
-SOURCES = ["kc_solve.cu", "kc_count.cu", "kc_tail.cu", "kc_peel.cu", "kc_prep.cu", "kc_api.cu", "kc_gen.cu", "kc_ingest.cu"]
+SOURCES = ["kc_solve.cu", "kc_count.cu", "kc_tail.cu", "kc_peel.cu", "kc_prep.cu", "kc_api.cu", "kc_gen.cu", "kc_ingest.cu", "kc_stage.cu"]
 HEADERS = ["kc_internal.h", "kc_dev.cuh", os.path.join("..", "..", "include", "kcore_b200.h")]
 
 

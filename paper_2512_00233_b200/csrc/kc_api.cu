@@ -12,7 +12,9 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <new>
 #include <string>
 #include <vector>
@@ -485,6 +487,13 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
   }
   uint64_t* d_off = nullptr;
   uint32_t* d_adj = nullptr;
+  struct Stage {  // the staged (pageable) neighbour upload's host thread
+    std::thread th;
+    std::mutex m;
+    std::condition_variable cv;
+    int recorded = 0;
+    cudaError_t err = cudaSuccess;
+  } stage;
   // pipelined neighbours (host path): chunks of old rows on a copy stream,
   // each relabelled by the layout as soon as it lands
   cudaStream_t cs = nullptr;
@@ -508,8 +517,14 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
       dfree(d_off, g->stream);
       return bail(cuda_fail(e, "cudaMallocAsync neighbors"));
     }
-    e = cudaMemcpyAsync(d_off, csr->offsets, ((size_t)g->n + 1) * sizeof(uint64_t),
-                        cudaMemcpyHostToDevice, g->stream);
+    // pageable host arrays (a reference Graph's std::vectors) go through the
+    // pinned staging ring (kc_stage.cu); pinned ones straight to the DMA engine
+    const bool pageable = is_pageable(csr->offsets) || is_pageable(csr->neighbors);
+    if (pageable)
+      e = staged_h2d(d_off, csr->offsets, ((size_t)g->n + 1) * sizeof(uint64_t), g->stream);
+    else
+      e = cudaMemcpyAsync(d_off, csr->offsets, ((size_t)g->n + 1) * sizeof(uint64_t),
+                          cudaMemcpyHostToDevice, g->stream);
     // chunks of ~64 MB of neighbours, cut at row boundaries (at most 16)
     const uint64_t bytes = g->nnz * sizeof(uint32_t);
     uint64_t k = (bytes + (64ull << 20) - 1) / (64ull << 20);
@@ -531,20 +546,45 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
     if (e == cudaSuccess) e = cudaEventRecord(alloc_done, g->stream);  // stream-ordered allocations
     if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, alloc_done, 0);
     if (alloc_done) cudaEventDestroy(alloc_done);
-    for (size_t c = 0; e == cudaSuccess && c + 1 < old_lo.size(); ++c) {
-      const uint64_t b0 = csr->offsets[old_lo[c]], b1 = csr->offsets[old_lo[c + 1]];
-      if (b1 > b0)
-        e = cudaMemcpyAsync(d_adj + b0, csr->neighbors + b0, (b1 - b0) * sizeof(uint32_t),
-                            cudaMemcpyHostToDevice, cs);
-      if (c == 0) hc.mark("H2D chunk 0 enqueued");
+    const size_t nchunks = old_lo.size() - 1;
+    for (size_t c = 0; e == cudaSuccess && c < nchunks; ++c) {
       cudaEvent_t ev = nullptr;
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-      if (e == cudaSuccess) {
-        ready.push_back(ev);
-        e = cudaEventRecord(ev, cs);
-      }
+      e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e == cudaSuccess) ready.push_back(ev);
     }
-    if (e == cudaSuccess) e = cudaEventRecord(g->ev[1], cs);
+    // chunk c: its neighbours on the copy stream, then ready[c]
+    auto copy_chunk = [&, cs](size_t c) -> cudaError_t {
+      const uint64_t b0 = csr->offsets[old_lo[c]], b1 = csr->offsets[old_lo[c + 1]];
+      cudaError_t ce = cudaSuccess;
+      if (b1 > b0)
+        ce = pageable ? staged_h2d(d_adj + b0, csr->neighbors + b0, (b1 - b0) * sizeof(uint32_t), cs)
+                      : cudaMemcpyAsync(d_adj + b0, csr->neighbors + b0,
+                                        (b1 - b0) * sizeof(uint32_t), cudaMemcpyHostToDevice, cs);
+      if (ce == cudaSuccess) ce = cudaEventRecord(ready[c], cs);
+      return ce;
+    };
+    if (e == cudaSuccess && !pageable) {
+      for (size_t c = 0; e == cudaSuccess && c < nchunks; ++c) e = copy_chunk(c);
+      if (e == cudaSuccess) e = cudaEventRecord(g->ev[1], cs);
+    } else if (e == cudaSuccess) {
+      // staged: a host thread fills the pinned ring chunk by chunk while this
+      // thread lays out the chunks already recorded (AdjFeed::host_wait)
+      stage.recorded = 0;
+      stage.err = cudaSuccess;
+      stage.th = std::thread([&, copy_chunk, nchunks] {
+        cudaSetDevice(g->device);
+        for (size_t c = 0; c < nchunks; ++c) {
+          cudaError_t ce = stage.err == cudaSuccess ? copy_chunk(c) : stage.err;
+          if (ce == cudaSuccess && c + 1 == nchunks) ce = cudaEventRecord(g->ev[1], cs);
+          {
+            std::lock_guard<std::mutex> lk(stage.m);
+            if (ce != cudaSuccess) stage.err = ce;
+            stage.recorded = (int)c + 1;
+          }
+          stage.cv.notify_all();
+        }
+      });
+    }
     if (e != cudaSuccess) {
       cudaStreamSynchronize(g->stream);
       if (cs) cudaStreamSynchronize(cs);
@@ -554,6 +594,14 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
       return bail(cuda_fail(e, "cudaMemcpy H2D"));
     }
     feed = AdjFeed{(int)ready.size(), old_lo.data(), ready.data()};
+    if (pageable) {
+      feed.host_wait = [](void* ctx, int c) {
+        Stage* st = static_cast<Stage*>(ctx);
+        std::unique_lock<std::mutex> lk(st->m);
+        st->cv.wait(lk, [&] { return st->recorded > c; });
+      };
+      feed.ctx = &stage;
+    }
     hc.mark("H2D enqueued");
   } else {
     d_off = const_cast<uint64_t*>(csr->offsets);
@@ -565,6 +613,10 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
                   (flags & KC_UPLOAD_UNSORTED_ROWS) == 0, g->stream, &g->lay,
                   on_device ? nullptr : &feed);
   hc.mark("layout returned");
+  if (stage.th.joinable()) {
+    stage.th.join();
+    if (stage.err != cudaSuccess && e == cudaSuccess) e = stage.err;
+  }
   if (cs) cudaStreamWaitEvent(g->stream, g->ev[1], 0);  // every chunk copied (error paths too)
   cudaEventRecord(g->ev[2], g->stream);
   cudaStreamSynchronize(g->stream);
@@ -725,12 +777,16 @@ static kc_status solve_impl(kc_graph* g, const kc_options* opt, uint32_t* out, b
   if (s != KC_OK) return s;
   if (out_dev)
     CK(cudaMemcpyAsync(out, g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, g->stream));
+  else if (g->n >= (1u << 20) && is_pageable(out))  // through the pinned ring (kc_stage.cu)
+    CK(staged_d2h(out, g->d_out, g->n * sizeof(uint32_t), g->stream));
   else
     CK(cudaMemcpyAsync(out, g->d_out, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
   CK(cudaEventRecord(g->ev[3], g->stream));
   CK(cudaStreamSynchronize(g->stream));
   hc.mark("solve: done");
   if (st) {
+    // init + rounds (+ tail list + tail) + k stats + permute-back
+    st->kernel_launches = 2u + (uses_tail(o) ? 2u : 0u) + 2u;
     cudaEventElapsedTime(&st->t_solve_ms, g->ev[0], g->ev[1]);
     cudaEventElapsedTime(&st->t_download_ms, g->ev[2], g->ev[3]);
   }

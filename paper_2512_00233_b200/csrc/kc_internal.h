@@ -197,7 +197,17 @@ struct AdjFeed {
   int k;
   const uint32_t* old_lo;
   const cudaEvent_t* ready;
+  // staged (pageable) uploads: ready[c] is recorded by a host thread; the
+  // layout first blocks until it has been (host_wait(ctx, c)), then waits on it
+  void (*host_wait)(void* ctx, int c) = nullptr;
+  void* ctx = nullptr;
 };
+
+// Pageable host memory (kc_stage.cu): copies through pinned staging slots
+// filled by host threads while the copy engine drains the previous slot.
+bool is_pageable(const void* p);
+cudaError_t staged_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
+cudaError_t staged_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, uint64_t nnz,
                         bool force_off64, bool sort_rows, cudaStream_t s, PrepOut* out,
                         const AdjFeed* feed = nullptr);

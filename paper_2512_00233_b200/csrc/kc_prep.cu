@@ -312,6 +312,7 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
     for (int c = 0; c < nparts; ++c) {
       const uint32_t o_lo = feed ? feed->old_lo[c] : 0u;
       const uint32_t o_hi = feed ? feed->old_lo[c + 1] : n;
+      if (feed && feed->host_wait) feed->host_wait(feed->ctx, c);  // recorded by the stager
       if (feed) PREP_CK(cudaStreamWaitEvent(s, feed->ready[c], 0));
       if (n_nz > n_big) {
         if (off64)

@@ -63,21 +63,25 @@ def test_clamped_start_hub_round_zero(gpu, oracle):
     assert st_c["h_graph"] < 30000
 
 
-def test_reference_rule_counters_repeatable(gpu, oracle):
+def test_reference_rule_counters_exact_and_repeatable(gpu, oracle):
     """Hub notify (kc_solve.cu notify_huge) applies E[u] = t only after a CTA
     barrier: with the degree cut a warp can finish its share of a hub row early,
     and before the barrier its store could reach a lagging warp's cap = E[u]
     load, which then skipped its notifications (a rare, timing-dependent
-    messages_sent deficit).  Repeated solves must give identical counters."""
-    for name, n, pairs in _graphs(oracle):
-        if name not in ("star_clique", "chunglu_hubs", "rmat15"):
-            continue
+    messages_sent deficit).  Every solve's RunReport must equal the CPU
+    Jacobi replay of the reference rule exactly (not just repeat itself): on
+    hub-heavy graphs whose hubs (degree > 8,192) take the CTA-wide notify
+    path with the degree cut active (sorted rows)."""
+    graphs = [(name, n, pairs) for name, n, pairs in _graphs(oracle)
+              if name in ("star_clique", "chunglu_hubs", "rmat15")]
+    graphs.append(("rmat18_hubs", 1 << 18, oracle.gen_rmat(18, 16, 21)))
+    for name, n, pairs in graphs:
         g = oracle.build_csr(n, pairs)
+        if name == "rmat18_hubs":
+            assert int(np.diff(g.off).max()) > 8192  # the CTA-wide hub path
+        want = oracle.jacobi(g, "ref_ext")["stats"]
         gg = gpu.GpuGraph(gpu.Graph(g.off, g.nbr))
         o = gpu.FastKOptions(rule=gpu.Rule.REFERENCE, hybrid_tail=False)
-        first = None
         for _ in range(25):
             _, st = gg.solve(o)
-            rep = {k: st[k] for k in KEYS}
-            first = first or rep
-            assert rep == first, name
+            assert {k: st[k] for k in KEYS} == {k: want[k] for k in KEYS}, name
