@@ -217,6 +217,11 @@ def measure(K, torch, cfg, args, local, steps, warmup, e2e_steps, dist=None, ws=
     ms_step = reduce_max(sum(ms) / len(ms), dist, device=f"cuda:{local}")
     st = stats[-1]
     launches = sum(int(x["kernel_launches"]) for x in stats)
+    # the gather ceiling of this graph: the solver's inner operation alone
+    # (id stream + one estimate gather per adjacency entry), same L2 flush
+    flush.fill_(1)
+    torch.cuda.synchronize()
+    probe_ms = gg.gather_probe(3)
     gg.free()
     del flush
     torch.cuda.synchronize()
@@ -253,7 +258,7 @@ def measure(K, torch, cfg, args, local, steps, warmup, e2e_steps, dist=None, ws=
                 ms_step=ms_step, wall=wall, clk=clk.summary(), launches=launches,
                 t_upload=t_upload, t_prep=t_prep, e2e_ms=e2e_ms, e2e_parts=e2e_parts,
                 e2e_pg_ms=e2e_pg_ms, e2e_pg_parts=e2e_pg_parts, pinned=pinned_ok,
-                e2e_steps=e2e_steps, ws=ws)
+                e2e_steps=e2e_steps, ws=ws, probe_ms=probe_ms)
 
 
 def roofline(m, rule):
@@ -262,10 +267,22 @@ def roofline(m, rule):
     bytes_alg = 8 * st["e_scan"] + 16 * st["v_eval"]
     achieved = bytes_alg / (m["ms_step"] * 1e-3) / 1e9
     kname = solver_kernel(rule)
+    # entries the solver actually streamed with a gather each (evaluate +
+    # notify phases), against the measured gather rate of the same graph
+    ent = int(st.get("scan_evaluate", 0)) + int(st.get("scan_notify", 0))
+    gather_rate = m["nnz"] / (m["probe_ms"] * 1e-3)
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": profile_traffic(m["cfg"], kname),
             "peak_source": peak_src, "kernel": f"{kname} (persistent)",
-            "bytes_alg_per_launch": bytes_alg}
+            "bytes_alg_per_launch": bytes_alg,
+            "gather_ceiling": {
+                "what": "kc_debug_gather_probe: id stream + one estimate gather per adjacency "
+                        "entry of this graph, nothing else (L2-bandwidth bound, ncu lts 80%)",
+                "probe_ms_per_pass": round(m["probe_ms"], 4),
+                "gathers_per_s": round(gather_rate / 1e9, 1), "unit": "G/s",
+                "solver_gathered_entries": ent or None,
+                "solver_time_at_ceiling_ms": round(ent / gather_rate * 1e3, 3) if ent else None,
+                "frac": round(ent / gather_rate * 1e3 / m["ms_step"], 4) if ent else None}}
 
 
 def e2e_obj(m):

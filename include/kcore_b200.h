@@ -95,7 +95,10 @@ typedef struct kc_stats {
   float t_solve_ms;          /* init -> converged estimates, CSR resident */
   float t_download_ms;       /* permute-back + D2H of the coreness */
   uint32_t kernel_launches;  /* this library's kernels launched by the call (solve path) */
-  uint32_t reserved[7];
+  uint32_t pad0;
+  uint64_t scan_evaluate;    /* entries streamed with a gather by evaluations (lists < rows) */
+  uint64_t scan_notify;      /* entries streamed with a gather by notify / pull scans */
+  uint32_t reserved[2];
 } kc_stats;
 
 /* A borrowed view of an undirected simple CSR: offsets has n+1 entries,
@@ -218,6 +221,10 @@ kc_status kc_debug_phase_times(kc_graph* g, unsigned long long* out, uint64_t ca
  * by notify, entries streamed by evaluate, queue sizes HUGE|BIG<<32,
  * WARP|SUB<<32, THREAD) for the first `rounds` rounds (at most 4096). */
 kc_status kc_debug_round_stats(kc_graph* g, unsigned long long* out, uint32_t rounds);
+/* Measurement probe (debug): `reps` passes of the solver's inner operation
+ * alone over every adjacency entry — the id stream plus one estimate gather
+ * each, no cache — after a solve; *ms_per_pass = device time per pass. */
+kc_status kc_debug_gather_probe(kc_graph* g, int reps, float* ms_per_pass);
 
 /* ---- synthetic inputs (BASELINE.json configs; the "kcgen v1" spec) ------ */
 /* Build one of the five configs (1..5) — or a scaled variant — directly on

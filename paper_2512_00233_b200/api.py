@@ -38,10 +38,12 @@ class _Stats(C.Structure):
                 ("tail_rounds", C.c_uint64), ("k_max", C.c_uint32), ("h_graph", C.c_uint32),
                 ("k_avg", C.c_double), ("t_upload_ms", C.c_float), ("t_prep_ms", C.c_float),
                 ("t_solve_ms", C.c_float), ("t_download_ms", C.c_float),
-                ("kernel_launches", C.c_uint32), ("reserved", C.c_uint32 * 7)]
+                ("kernel_launches", C.c_uint32), ("pad0", C.c_uint32),
+                ("scan_evaluate", C.c_uint64), ("scan_notify", C.c_uint64),
+                ("reserved", C.c_uint32 * 2)]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        return {k: getattr(self, k) for k, _ in self._fields_ if k not in ("reserved", "pad0")}
 
 
 class _CSRView(C.Structure):
@@ -67,7 +69,7 @@ ABI_SYMBOLS = (
     "kc_graph_nnz", "kc_graph_timings", "kc_solve", "kc_solve_device",
     "kc_solve_observed", "kc_fastk_run", "kc_graph_stream", "kc_gen_config",
     "kc_csr_dev_free", "kc_csr_dev_download", "kc_debug_phase_times", "kc_graph_upload_ex",
-    "kc_debug_round_stats", "kc_solve_traced", "kc_peel", "kc_verify", "kc_load_edge_list",
+    "kc_debug_round_stats", "kc_debug_gather_probe", "kc_solve_traced", "kc_peel", "kc_verify", "kc_load_edge_list",
     "kc_load_edge_list_file", "kc_csr_dev_original_ids", "kc_sequential_tail",
 )
 KC_DEBUG_PHASE_TIMES = 1
@@ -154,6 +156,8 @@ def load_library():
                                        C.POINTER(C.c_uint32)]
     L.kc_debug_round_stats.restype = C.c_int
     L.kc_debug_round_stats.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32]
+    L.kc_debug_gather_probe.restype = C.c_int
+    L.kc_debug_gather_probe.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_float)]
     L.kc_csr_dev_download.restype = C.c_int
     L.kc_csr_dev_download.argtypes = [C.POINTER(_CSRDev), C.c_void_p, C.c_void_p]
     _lib = L
@@ -561,6 +565,14 @@ class GpuGraph:
         _check(load_library().kc_debug_phase_times(self._h, buf.ctypes.data, buf.size,
                                                    C.byref(grid)), "kc_debug_phase_times")
         return buf[: 256 * grid.value * 8].reshape(256, grid.value, 8)
+
+    def gather_probe(self, reps: int = 3) -> float:
+        """ms per pass of the solver's inner operation alone (id stream + one
+        estimate gather per adjacency entry; kc_debug_gather_probe)."""
+        ms = C.c_float()
+        _check(load_library().kc_debug_gather_probe(self._h, reps, C.byref(ms)),
+               "kc_debug_gather_probe")
+        return ms.value
 
     def round_stats(self, rounds: int) -> np.ndarray:
         """[rounds, 9] per-round counters of the last solve (debug): evals,

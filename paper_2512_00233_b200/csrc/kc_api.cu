@@ -123,6 +123,32 @@ __global__ void permute_back_kernel(const void* est, bool est16, const uint32_t*
   }
 }
 
+// Measurement probe (kc_debug_gather_probe): one pass over every adjacency
+// entry of the layout — the 128-bit id stream with the solver's L2
+// evict-first hint, and one gather of the entry's estimate from `est` (no
+// shared-memory cache) — i.e. the solver's inner operation with nothing
+// else.  Its ncu L2 hit rate, with the id sectors (read once: misses)
+// taken out, is the hit rate of the estimate gathers; its time is the
+// gather rate this graph allows.
+template <typename EstT>
+__global__ void est_gather_probe_kernel(const uint32_t* __restrict__ adj, uint64_t nnz,
+                                        const EstT* __restrict__ est,
+                                        unsigned long long* out) {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  const uint64_t nvec = nnz / 4;
+  uint32_t acc = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 q;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
+                 : "l"(adj + 4 * i), "l"(pol));
+    acc += (uint32_t)est[q.x] + (uint32_t)est[q.y] + (uint32_t)est[q.z] + (uint32_t)est[q.w];
+  }
+  if (acc == 0x7fffffffu) atomicAdd(out, 1ull);  // keeps the loads
+}
+
 template <typename OffT>
 __global__ void degree_back_kernel(const OffT* off, const uint32_t* perm, uint32_t n,
                                    uint32_t n_nz, uint32_t* out) {
@@ -389,7 +415,10 @@ kc_status collect(kc_graph* g, const kc_options& o, kc_stats* st, bool* converge
     CK(cudaMemcpy(rs.data(), g->sb.stats, slots * sizeof(RoundStat), cudaMemcpyDeviceToHost));
   st->iterations = rounds;
   st->messages_sent = st->messages_drained = st->e_scan = st->v_eval = st->drops = 0;
+  st->scan_evaluate = st->scan_notify = 0;
   for (const RoundStat& r : rs) {
+    st->scan_evaluate += r.ascan;
+    st->scan_notify += r.nscan;
     st->messages_sent += r.fires;
     st->v_eval += r.evals;
     st->e_scan += r.escan;
@@ -995,6 +1024,30 @@ kc_status kc_debug_round_stats(kc_graph* g, unsigned long long* out, uint32_t ro
   if (!g->sb.stats) return fail(KC_ERR_INVALID_ARGUMENT, "no solve has run");
   const uint32_t k = rounds < STAT_SLOTS ? rounds : STAT_SLOTS;
   CK(cudaMemcpy(out, g->sb.stats, (size_t)k * sizeof(RoundStat), cudaMemcpyDeviceToHost));
+  return KC_OK;
+}
+
+kc_status kc_debug_gather_probe(kc_graph* g, int reps, float* ms_per_pass) {
+  kcb::DeviceGuard device_guard;
+  if (!g || !ms_per_pass) return fail(KC_ERR_INVALID_ARGUMENT, "null argument");
+  if (!g->sb.est[0]) return fail(KC_ERR_INVALID_ARGUMENT, "no solve has run");
+  CK(cudaSetDevice(g->device));
+  const uint64_t nnz = g->nnz & ~(uint64_t)3;
+  CK(cudaEventRecord(g->ev[0], g->stream));
+  for (int r = 0; r < (reps > 0 ? reps : 1); ++r) {
+    if (g->est16)
+      est_gather_probe_kernel<uint16_t><<<g->num_sms * 8, 256, 0, g->stream>>>(
+          g->lay.adj, nnz, (const uint16_t*)g->sb.est[0], g->d_count);
+    else
+      est_gather_probe_kernel<uint32_t><<<g->num_sms * 8, 256, 0, g->stream>>>(
+          g->lay.adj, nnz, (const uint32_t*)g->sb.est[0], g->d_count);
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(g->ev[1], g->stream));
+  CK(cudaEventSynchronize(g->ev[1]));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]);
+  *ms_per_pass = ms / (reps > 0 ? reps : 1);
   return KC_OK;
 }
 
