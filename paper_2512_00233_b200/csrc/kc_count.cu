@@ -1831,8 +1831,12 @@ __device__ __noinline__ void pull_phase(const CP<OffT, EstT>& p, const View<EstT
                                         Ctl& ctl, const EstT* s_cache, uint32_t* s_hist,
                                         uint32_t* w_bins, FlatW& fw, const uint32_t* s_dcut,
                                         Acc& acc) {
-  eval_phase<true>(p, v, sh, ctl, 1, s_cache, s_hist, w_bins, fw, s_dcut,
-                   (unsigned long long*)nullptr, acc);
+  // phase stamps of PULL (debug): the last profile row, slots 1-4
+  unsigned long long* pf = (p.prof && threadIdx.x == 0)
+                               ? p.prof + ((size_t)(PROF_ROUNDS - 1) * gridDim.x + blockIdx.x) * PROF_PHASES
+                               : nullptr;
+  if (pf) pf[1] = gtimer();
+  eval_phase<true>(p, v, sh, ctl, 1, s_cache, s_hist, w_bins, fw, s_dcut, pf, acc);
 }
 
 // After PULL: the flagged round-1 droppers become round 1's queue (class

@@ -39,5 +39,10 @@ for r in range(R):
     qs = [q[6] & 0xffffffff, q[6] >> 32, q[7] & 0xffffffff, q[7] >> 32, q[8]]
     print(f"{r:5d} {(pt[r,:,0].min()-t0)/1e3:9.1f}  " + " ".join(f"{x:10.1f}" for x in mx) +
           f"   | {q[0]:8d} {q[1]/1e6:8.2f} {q[5]/1e6:8.2f} {q[4]/1e6:8.2f} {q[3]/1e6:8.2f}  " + " ".join(str(int(v)) for v in qs))
+pr = pt[255]
+if pr[:, 1].max() > 0:  # PULL's phases (kc_count.cu pull_phase)
+    d = np.diff(pr[:, 1:5], axis=1) / 1e3
+    mx = d.max(axis=0)
+    print("PULL phases (max over CTAs, us): huge %.1f  big+warp %.1f  sub+thread+long %.1f" % tuple(mx))
 print("totals: escan %.1fM ascan %.1fM nscan %.1fM" % (rs[:,1].sum()/1e6, rs[:,5].sum()/1e6, rs[:,4].sum()/1e6))
 print("sum of max:", " ".join(f"{n}={x:.0f}" for n, x in zip(names, tot)))
