@@ -1812,16 +1812,18 @@ __device__ __forceinline__ void eval_phase(const CP<OffT, EstT>& p, const View<E
   consume_long(p, v, sh, ctl, ph, false, eval_long);
   if (pf) pf[2] = gtimer();
   KC_BOUNDS(blockDim.x == SOLVE_THREADS);
+  // (empty classes skip the out-of-line calls: their prologues and epilogues
+  // cost ~1 us each in the small rounds, scripts/round_overhead.py)
   if (v.r0 || PULL || !KC_FLAT_EVAL) {
-    eval_wclass<PULL>(p, v, s_cache, w_bins, C_BIG, GMAX_BIG, acc);
-    eval_wclass<PULL>(p, v, s_cache, w_bins, C_WARP, GMAX_WARP, acc);
+    if (v.qcnt[C_BIG]) eval_wclass<PULL>(p, v, s_cache, w_bins, C_BIG, GMAX_BIG, acc);
+    if (v.qcnt[C_WARP]) eval_wclass<PULL>(p, v, s_cache, w_bins, C_WARP, GMAX_WARP, acc);
   } else {
-    flat_eval(p, v, s_cache, w_bins, fw, C_BIG, GMAX_BIG, acc);
-    flat_eval(p, v, s_cache, w_bins, fw, C_WARP, GMAX_WARP, acc);
+    if (v.qcnt[C_BIG]) flat_eval(p, v, s_cache, w_bins, fw, C_BIG, GMAX_BIG, acc);
+    if (v.qcnt[C_WARP]) flat_eval(p, v, s_cache, w_bins, fw, C_WARP, GMAX_WARP, acc);
   }
   if (pf) pf[3] = gtimer();
-  eval_sub<PULL>(p, v, s_cache, s_dcut, acc);
-  eval_thread<PULL>(p, v, s_cache, s_dcut, acc);
+  if (v.qcnt[C_SUB]) eval_sub<PULL>(p, v, s_cache, s_dcut, acc);
+  if (v.qcnt[C_THREAD]) eval_thread<PULL>(p, v, s_cache, s_dcut, acc);
   consume_long(p, v, sh, ctl, ph, true, eval_long);
   if (pf) pf[4] = gtimer();
 }
@@ -2075,16 +2077,16 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     });
     consume_long(p, v, sh, ctl, 1, false, notify_long);
     if (v.r0 || !KC_FLAT_NOTIFY) {
-      notify_wclass(p, v, q, s_cache, w_bins, C_BIG, GMAX_BIG, acc);
-      notify_wclass(p, v, q, s_cache, w_bins, C_WARP, GMAX_WARP, acc);
+      if (v.qcnt[C_BIG]) notify_wclass(p, v, q, s_cache, w_bins, C_BIG, GMAX_BIG, acc);
+      if (v.qcnt[C_WARP]) notify_wclass(p, v, q, s_cache, w_bins, C_WARP, GMAX_WARP, acc);
     } else {
-      flat_notify(p, v, q, s_cache, w_bins, s_flat[warp_id()], C_BIG, GMAX_BIG, acc);
-      flat_notify(p, v, q, s_cache, w_bins, s_flat[warp_id()], C_WARP, GMAX_WARP, acc);
+      if (v.qcnt[C_BIG]) flat_notify(p, v, q, s_cache, w_bins, s_flat[warp_id()], C_BIG, GMAX_BIG, acc);
+      if (v.qcnt[C_WARP]) flat_notify(p, v, q, s_cache, w_bins, s_flat[warp_id()], C_WARP, GMAX_WARP, acc);
     }
-    notify_small(p, v, q, s_cache, C_SUB, acc);
-    notify_thread(p, v, q, s_cache, acc);
+    if (v.qcnt[C_SUB]) notify_small(p, v, q, s_cache, C_SUB, acc);
+    if (v.qcnt[C_THREAD]) notify_thread(p, v, q, s_cache, acc);
     consume_long(p, v, sh, ctl, 1, true, notify_long);
-    wq_flush_all(p, q);
+    if (__any_sync(FULL, lane_id() < (uint32_t)NCLS && wn[lane_id()] != 0u)) wq_flush_all(p, q);
     flush_acc(p, sr, acc, sh.acc);
     grid.sync();
     if (pf) pf[7] = gtimer();
