@@ -257,8 +257,9 @@ typedef struct kc_parse_error {
 } kc_parse_error;
 kc_status kc_load_edge_list(const char* text, uint64_t len, int device, kc_csr_dev** out,
                             kc_parse_error* err);
-/* Same from a plain-text file (gzip input is out of scope: no zlib in the
- * product); KC_ERR_IO if it cannot be read. */
+/* Same from a file, gzip-compressed or plain (zlib's gzopen, as the
+ * reference's load_edge_list_file, graph.cpp:200-226); KC_ERR_IO with the
+ * reference's message if it cannot be opened or read. */
 kc_status kc_load_edge_list_file(const char* path, int device, kc_csr_dev** out,
                                  kc_parse_error* err);
 /* Host copy of the original ids of a device CSR (n entries). */

@@ -70,7 +70,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
                 raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
     if force or jobs or _stale(lib, objs):
         cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib] + objs + \
-              ["-Xcompiler", "-fPIC", "-cudart", "static"]
+              ["-Xcompiler", "-fPIC", "-cudart", "static", "-lz"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

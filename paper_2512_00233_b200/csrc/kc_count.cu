@@ -1105,7 +1105,10 @@ __device__ __noinline__ void eval_sub(const CP<OffT, EstT>& p, const View<EstT>&
 #define KC_TU 2
 #endif
 constexpr int TU = KC_TU;                       // evaluate: vertices per lane per pass
-constexpr int TUN = 2;                          // notify: droppers per lane per pass
+#ifndef KC_TUN
+#define KC_TUN 2
+#endif
+constexpr int TUN = KC_TUN;                     // notify: droppers per lane per pass
 constexpr uint32_t GMAX_THREAD = 32u * TU * 4u;  // ids per grab (max)
 
 __device__ __forceinline__ uint32_t warp_grab(uint32_t* cursor, uint32_t cnt, uint32_t G) {

@@ -30,6 +30,8 @@
 #include "../../include/kcore_b200.h"
 #include "kc_internal.h"
 
+#include <zlib.h>
+
 namespace kcb {
 
 // kc_gen.cu
@@ -333,21 +335,29 @@ kc_status kc_load_edge_list_file(const char* path, int device, kc_csr_dev** out,
                                  kc_parse_error* err) {
   if (!out || !path) return KC_ERR_INVALID_ARGUMENT;
   *out = nullptr;
-  FILE* f = std::fopen(path, "rb");
-  if (!f) {
+  // kcore::load_edge_list_file (graph.cpp:200-226): gzopen reads gzip-compressed
+  // and plain files alike; the same IoError messages
+  gzFile gz = gzopen(path, "rb");
+  if (!gz) {
     kcb::set_parse_error(err, 0, std::string("cannot open '") + path + "': " + std::strerror(errno));
     return KC_ERR_IO;
   }
+  gzbuffer(gz, 1 << 20);
   std::vector<char> buf;
-  char chunk[1 << 16];
-  size_t got;
-  while ((got = std::fread(chunk, 1, sizeof(chunk), f)) > 0) buf.insert(buf.end(), chunk, chunk + got);
-  const bool bad = std::ferror(f) != 0;
-  std::fclose(f);
-  if (bad) {
-    kcb::set_parse_error(err, 0, std::string("error reading '") + path + "'");
-    return KC_ERR_IO;
+  std::vector<char> chunk(1 << 20);
+  for (;;) {
+    const int got = gzread(gz, chunk.data(), (unsigned)chunk.size());
+    if (got < 0) {
+      int errnum = 0;
+      const char* msg = gzerror(gz, &errnum);
+      kcb::set_parse_error(err, 0, std::string("error reading '") + path + "': " + msg);
+      gzclose(gz);
+      return KC_ERR_IO;
+    }
+    if (got == 0) break;
+    buf.insert(buf.end(), chunk.data(), chunk.data() + got);
   }
+  gzclose(gz);
   return kcb::ingest(buf.data(), buf.size(), device, out, err);
 }
 

@@ -72,3 +72,26 @@ def test_file_and_io_error(gpu, tmp_path):
     check_graph(gpu.load_edge_list_file(str(p)), want)
     with pytest.raises(gpu.IoError):
         gpu.load_edge_list_file(str(tmp_path / "missing.txt"))
+
+
+def test_gzip_file_like_the_reference(gpu, tmp_path):
+    """load_edge_list_file reads gzip input transparently (graph.cpp:200-226):
+    the same CSR and original ids as the plain text, for every golden case;
+    malformed compressed input raises ParseError / IoError like the text."""
+    import gzip
+    cases = golden("edge_lists.json")
+    for name, want in cases.items():
+        p = tmp_path / f"{name}.txt.gz"
+        with gzip.open(p, "wb") as f:
+            f.write(want["text"].encode())
+        if "error" in want:
+            with pytest.raises(gpu.ParseError) as e:
+                gpu.load_edge_list_file(str(p))
+            assert e.value.line == want["error_line"]
+        else:
+            check_graph(gpu.load_edge_list_file(str(p)), want)
+    bad = tmp_path / "truncated.gz"
+    data = gzip.compress(cases["random_3000"]["text"].encode())
+    bad.write_bytes(data[: len(data) // 2])
+    with pytest.raises((gpu.IoError, gpu.ParseError)):
+        gpu.load_edge_list_file(str(bad))
