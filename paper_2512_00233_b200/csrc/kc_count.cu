@@ -808,7 +808,11 @@ __device__ __forceinline__ void eval_wclass_impl(const CP<OffT, EstT>& p, const 
                             uint32_t* bins, int c, uint32_t gmax, A& acc) {
   for_class(p, v, c, gmax, [&](uint32_t u, uint32_t n) {
     Item mine{};
-    if (lane_id() < n) mine = eval_item<PULL>(p, v, s_cache, u);
+    if (lane_id() < n) {
+      mine = eval_item<PULL>(p, v, s_cache, u);
+      if (!mine.spec && !(KC_R0_SORTED && v.r0 && p.dc.sorted))  // (round 0 sorted: a prefix)
+        l2_prefetch_ids((mine.list ? (const uint32_t*)p.radj : p.adj) + mine.ob, mine.len);
+    }
     for (uint32_t i = 0; i < n; ++i) {
       Item it;
       it.u = __shfl_sync(FULL, mine.u, i);
@@ -923,6 +927,7 @@ __device__ __forceinline__ void flat_eval_impl(const CP<OffT, EstT>& p, const Vi
     uint32_t L = 0;
     if (lane < n) {
       it = eval_item<false>(p, v, s_cache, u);
+      if (!it.spec) l2_prefetch_ids((it.list ? (const uint32_t*)p.radj : p.adj) + it.ob, it.len);
       L = it.lo;
       if (it.list && it.thr > L) L = it.thr;
       if (it.cap > fb && it.cap - fb > L) L = it.cap - fb;
@@ -1489,7 +1494,11 @@ __device__ __forceinline__ void notify_wclass_impl(const CP<OffT, EstT>& p, cons
   unsigned long long nscan = 0;
   for_class(p, v, c, gmax, [&](uint32_t u, uint32_t n) {
     Drop mine{};
-    if (lane_id() < n) mine = drop_item(p, u);
+    if (lane_id() < n) {
+      mine = drop_item(p, u);
+      if (mine.t < mine.cap)
+        l2_prefetch_ids((mine.thr ? (const uint32_t*)p.radj : p.adj) + mine.ob, mine.len);
+    }
     for (uint32_t i = 0; i < n; ++i) {
       Drop d;
       d.t = __shfl_sync(FULL, mine.t, i);

@@ -169,6 +169,29 @@ __device__ __forceinline__ uint4 ld_ids4(const uint32_t* src, uint64_t a) {  // 
 #endif
   return r;
 }
+// Bulk L2 prefetch of a row / list by the copy engine (cp.async.bulk.prefetch,
+// sm_90+): one instruction per item, no registers held while it is in flight.
+// The solver's chains start with a DRAM round trip for each queued vertex's
+// first ids (the CSR and the lists do not fit L2); issuing the prefetch for
+// every item of a grab as soon as its metadata is known turns those into L2
+// hits.  KC_L2_PREFETCH=0 disables (A/B).
+#ifndef KC_L2_PREFETCH
+#define KC_L2_PREFETCH 1
+#endif
+__device__ __forceinline__ void l2_prefetch_ids(const uint32_t* p, uint64_t n) {
+#if KC_L2_PREFETCH
+  const uint64_t a = reinterpret_cast<uint64_t>(p) & ~(uint64_t)15;
+  const uint64_t b = (reinterpret_cast<uint64_t>(p + n) + 15) & ~(uint64_t)15;
+  uint64_t bytes = b - a;
+  if (bytes > (1u << 20)) bytes = 1u << 20;  // the head of a hub row is enough
+  if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)bytes)
+                      : "memory");
+#else
+  (void)p;
+  (void)n;
+#endif
+}
+
 __device__ __forceinline__ uint32_t u4_get(const uint4& q, int e) {
   return e == 0 ? q.x : e == 1 ? q.y : e == 2 ? q.z : q.w;
 }
