@@ -1917,7 +1917,7 @@ template <typename OffT, typename EstT>
 __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __grid_constant__ CP<OffT, EstT> p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem[];
-  EstT* s_cache = reinterpret_cast<EstT*>(smem);
+  EstT* s_cache = opaque_ptr(reinterpret_cast<EstT*>(smem));  // see opaque_ptr
   const size_t cache_bytes = ((size_t)p.cache_n * sizeof(EstT) + 15) & ~(size_t)15;
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(smem + cache_bytes);  // CTA window / warp bins
   uint32_t* w_bins = s_hist + WARP_BINS * warp_id();

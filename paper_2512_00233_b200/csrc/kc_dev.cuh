@@ -52,6 +52,26 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // Estimate of v: shared-memory cache for the highest-degree ids, global
 // (L1/L2) otherwise.  One generic load per gather keeps the inlined gather
 // sites small for the instruction cache.
+// The estimate cache's generic address, opaque to the compiler.  Left as a
+// pointer the compiler knows to be shared, it rebuilds the generic address
+// of the shared window (S2R SR_CgaCtaId + S2R SR_SWINHI + LEA + MOVs) at
+// every gather site instead of keeping it in a register: ~9 extra
+// instructions, two of them slow special-register reads, per gathered
+// estimate (SASS of the notify scans).  KC_OPAQUE_CACHE=0 restores that.
+#ifndef KC_OPAQUE_CACHE
+#define KC_OPAQUE_CACHE 1
+#endif
+template <typename T>
+__device__ __forceinline__ T* opaque_ptr(T* p) {
+#if KC_OPAQUE_CACHE
+  T* r;
+  asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(p));
+  return r;
+#else
+  return p;
+#endif
+}
+
 #ifndef KC_EST_CACHE
 #define KC_EST_CACHE 1   // 0: every gather from global memory (A/B: R-MAT 22 -1.5%,
                          // R-MAT 26 +1.6%; explicit LDS/LDG pairs cost more)

@@ -695,7 +695,7 @@ template <typename OffT, typename EstT>
 __global__ void __launch_bounds__(SOLVE_THREADS, KC_CTAS_PER_SM) rounds_kernel(P<OffT, EstT> p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem[];
-  EstT* s_cache = reinterpret_cast<EstT*>(smem);
+  EstT* s_cache = opaque_ptr(reinterpret_cast<EstT*>(smem));  // see opaque_ptr
   const size_t cache_bytes = ((size_t)p.cache_n * sizeof(EstT) + 15) & ~(size_t)15;
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(smem + cache_bytes);
   // per-warp regions (alias s_hist once the HUGE phase is over):
