@@ -44,6 +44,7 @@
 // An empty queue at a round start is the quiescent round: converged.
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <mutex>
 
 #include "kc_dev.cuh"
 #include "kc_internal.h"
@@ -177,6 +178,17 @@ struct CP {
   bool pull;            // round 0 ends with the PULL phase (see the kernel)
 };
 
+// The solver's parameters in constant memory, for the out-of-line phase
+// functions: a `const CP&` argument is a generic pointer there, and every
+// field it reads (the counter array of each atomic, the estimate arrays of
+// each stream) was a generic load with a uniform-descriptor move (LD.E +
+// R2UR pairs in SASS).  From the constant bank they are LDC / ULDC.  Written
+// by launch_t right before the launch, ordered after the previous solve's
+// kernel on any stream (c_done), so concurrent solves never see each
+// other's copy.
+template <typename OffT, typename EstT>
+__constant__ CP<OffT, EstT> c_params;
+
 template <typename EstT>
 struct View {
   const EstT* snap;      // gathered estimates: E (evaluate) or N (notify)
@@ -301,7 +313,9 @@ struct Enq {            // the warp's view of the next round's queue
 };
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ void wq_flush(const CP<OffT, EstT>& p, const Enq& q, int c) {
+__device__ __noinline__ void wq_flush(const CP<OffT, EstT>& p_arg, const Enq& q, int c) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   const uint32_t n = q.wn[c];
   if (n == 0) return;
   uint32_t base = 0;
@@ -319,7 +333,9 @@ __device__ __noinline__ void wq_flush(const CP<OffT, EstT>& p, const Enq& q, int
 // atomics of all classes in flight together (lane c reserves class c), one
 // round trip instead of one per non-empty class.
 template <typename OffT, typename EstT>
-__device__ __noinline__ void wq_flush_all(const CP<OffT, EstT>& p, const Enq& q) {
+__device__ __noinline__ void wq_flush_all(const CP<OffT, EstT>& p_arg, const Enq& q) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   const uint32_t lane = lane_id();
   uint32_t n = lane < (uint32_t)NCLS ? q.wn[lane] : 0u;
   uint32_t base = 0;
@@ -339,7 +355,9 @@ __device__ __noinline__ void wq_flush_all(const CP<OffT, EstT>& p, const Enq& q)
 
 // One activation per lane at most (a: this lane activates `id`).
 template <typename OffT, typename EstT>
-__device__ __noinline__ void wq_push(const CP<OffT, EstT>& p, const Enq& q, bool a, uint32_t id) {
+__device__ __noinline__ void wq_push(const CP<OffT, EstT>& p_arg, const Enq& q, bool a, uint32_t id) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   const int c = a ? cls_of(p, id) : NCLS;
 #pragma unroll 1
   for (int cc = 0; cc < NCLS; ++cc) {
@@ -685,8 +703,10 @@ __device__ __forceinline__ void eval_warp(const CP<OffT, EstT>& p, const View<Es
 }
 
 template <bool PULL, typename OffT, typename EstT>
-__device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+__device__ __noinline__ void eval_cta(const CP<OffT, EstT>& p_arg, const View<EstT>& v, const EstT* s_cache,
                          uint32_t* s_hist, Shared& sh, uint32_t u, Acc& acc) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   const Item it = eval_item<PULL>(p, v, s_cache, u);
   if (it.spec) {
     if (threadIdx.x == 0) finish_eval<PULL>(p, v, it, it.spec_t, it.spec_c, 0u, acc);
@@ -834,8 +854,10 @@ __device__ __forceinline__ void eval_wclass_impl(const CP<OffT, EstT>& p, const 
 // Counters in registers for the whole phase (an Acc& into the kernel's
 // frame would be local-memory traffic per evaluation).
 template <bool PULL, typename OffT, typename EstT>
-__device__ __noinline__ void eval_wclass(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+__device__ __noinline__ void eval_wclass(const CP<OffT, EstT>& p_arg, const View<EstT>& v, const EstT* s_cache,
                             uint32_t* bins, int c, uint32_t gmax, Acc& acc) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   Acc32 a{0, 0, 0, 0, 0, 0, false};
   eval_wclass_impl<PULL>(p, v, s_cache, bins, c, gmax, a);
   merge_acc(acc, a);
@@ -998,9 +1020,11 @@ __device__ __forceinline__ void flat_eval_impl(const CP<OffT, EstT>& p, const Vi
 }
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ void flat_eval(const CP<OffT, EstT>& p, const View<EstT>& v,
+__device__ __noinline__ void flat_eval(const CP<OffT, EstT>& p_arg, const View<EstT>& v,
                                        const EstT* s_cache, uint32_t* bins, FlatW& fw, int c,
                                        uint32_t gmax, Acc& acc) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   Acc32 a{0, 0, 0, 0, 0, 0, false};
   flat_eval_impl(p, v, s_cache, bins, fw, c, gmax, a);
   merge_acc(acc, a);
@@ -1093,8 +1117,10 @@ __device__ __forceinline__ void eval_sub_impl(const CP<OffT, EstT>& p, const Vie
 }
 
 template <bool PULL, typename OffT, typename EstT>
-__device__ __noinline__ void eval_sub(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+__device__ __noinline__ void eval_sub(const CP<OffT, EstT>& p_arg, const View<EstT>& v, const EstT* s_cache,
                          const uint32_t* s_dcut, Acc& acc) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   Acc32 a{0, 0, 0, 0, 0, 0, false};
   eval_sub_impl<PULL>(p, v, s_cache, s_dcut, a);
   merge_acc(acc, a);
@@ -1223,8 +1249,10 @@ __device__ __forceinline__ void eval_thread_impl(const CP<OffT, EstT>& p, const 
 }
 
 template <bool PULL, typename OffT, typename EstT>
-__device__ __noinline__ void eval_thread(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
+__device__ __noinline__ void eval_thread(const CP<OffT, EstT>& p_arg, const View<EstT>& v, const EstT* s_cache,
                             const uint32_t* s_dcut, Acc& acc) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   Acc32 a{0, 0, 0, 0, 0, 0, false};
   eval_thread_impl<PULL>(p, v, s_cache, s_dcut, a);
   merge_acc(acc, a);
@@ -1324,11 +1352,13 @@ __device__ __forceinline__ uint32_t notify_warp(const CP<OffT, EstT>& p, const E
 }
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p, const Enq& q,
+__device__ __noinline__ uint32_t notify_cta(const CP<OffT, EstT>& p_arg, const Enq& q,
                                             const EstT* s_cache, uint32_t cache_n, Shared& sh,
                                             uint32_t* s_hist, const uint32_t* src, bool ro, uint32_t u,
                                             uint64_t ob, uint32_t len, uint32_t t, uint32_t cap,
                                             uint32_t build, uint32_t tag, uint32_t floor) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   const uint32_t tid = threadIdx.x;
   if (tid == 0) sh.cursor = 0;
   // the CTA has HIST_BINS bins: a hub's next-round window reaches that far
@@ -1429,11 +1459,13 @@ struct Drop {
 };
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ uint32_t notify_row_warp(const CP<OffT, EstT>& p, const Enq& q,
+__device__ __noinline__ uint32_t notify_row_warp(const CP<OffT, EstT>& p_arg, const Enq& q,
                                                  const EstT* s_cache, uint32_t cache_n,
                                                  uint32_t* bins, uint32_t u, uint64_t ob,
                                                  uint32_t len, uint32_t t, uint32_t cap,
                                                  uint32_t build, uint32_t tag) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   return notify_warp<true>(p, q, s_cache, cache_n, bins, p.adj, true, u, ob, len, t, cap, build,
                            tag, KC_ROW_FLOOR_BUILD && build ? build : 1u);
 }
@@ -1518,9 +1550,11 @@ __device__ __forceinline__ void notify_wclass_impl(const CP<OffT, EstT>& p, cons
 }
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p, const View<EstT>& v,
+__device__ __noinline__ void notify_wclass(const CP<OffT, EstT>& p_arg, const View<EstT>& v,
                                            const Enq& q, const EstT* s_cache, uint32_t* bins,
                                            int c, uint32_t gmax, Acc& acc) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   Acc32 a{0, 0, 0, 0, 0, 0, false};
   notify_wclass_impl(p, v, q, s_cache, bins, c, gmax, a);
   merge_acc(acc, a);
@@ -1642,9 +1676,11 @@ __device__ __forceinline__ void flat_notify_impl(const CP<OffT, EstT>& p, const 
 }
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ void flat_notify(const CP<OffT, EstT>& p, const View<EstT>& v,
+__device__ __noinline__ void flat_notify(const CP<OffT, EstT>& p_arg, const View<EstT>& v,
                                          const Enq& q, const EstT* s_cache, uint32_t* bins,
                                          FlatW& fw, int c, uint32_t gmax, Acc& acc) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   Acc32 a{0, 0, 0, 0, 0, 0, false};
   flat_notify_impl(p, v, q, s_cache, bins, fw, c, gmax, a);
   merge_acc(acc, a);
@@ -1700,8 +1736,10 @@ __device__ __forceinline__ void notify_small_impl(const CP<OffT, EstT>& p, const
 }
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ void notify_small(const CP<OffT, EstT>& p, const View<EstT>& v,
+__device__ __noinline__ void notify_small(const CP<OffT, EstT>& p_arg, const View<EstT>& v,
                                           const Enq& q, const EstT* s_cache, int c, Acc& acc) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   Acc32 a{0, 0, 0, 0, 0, 0, false};
   notify_small_impl(p, v, q, s_cache, c, a);
   merge_acc(acc, a);
@@ -1778,8 +1816,10 @@ __device__ __forceinline__ void notify_thread_impl(const CP<OffT, EstT>& p, cons
 }
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ void notify_thread(const CP<OffT, EstT>& p, const View<EstT>& v,
+__device__ __noinline__ void notify_thread(const CP<OffT, EstT>& p_arg, const View<EstT>& v,
                                            const Enq& q, const EstT* s_cache, Acc& acc) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   Acc32 a{0, 0, 0, 0, 0, 0, false};
   notify_thread_impl(p, v, q, s_cache, a);
   merge_acc(acc, a);
@@ -1841,10 +1881,12 @@ __device__ __forceinline__ void eval_phase(const CP<OffT, EstT>& p, const View<E
 }
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ void pull_phase(const CP<OffT, EstT>& p, const View<EstT>& v, Shared& sh,
+__device__ __noinline__ void pull_phase(const CP<OffT, EstT>& p_arg, const View<EstT>& v, Shared& sh,
                                         Ctl& ctl, const EstT* s_cache, uint32_t* s_hist,
                                         uint32_t* w_bins, FlatW& fw, const uint32_t* s_dcut,
                                         Acc& acc) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   // phase stamps of PULL (debug): the last profile row, slots 1-4
   unsigned long long* pf = (p.prof && threadIdx.x == 0)
                                ? p.prof + ((size_t)(PROF_ROUNDS - 1) * gridDim.x + blockIdx.x) * PROF_PHASES
@@ -1861,8 +1903,10 @@ __device__ __noinline__ void pull_phase(const CP<OffT, EstT>& p, const View<EstT
 constexpr uint32_t PULL_IDS = SOLVE_THREADS * 16;
 
 template <typename OffT, typename EstT>
-__device__ __noinline__ void compact_pull(const CP<OffT, EstT>& p, uint32_t* qcnt, uint32_t* queue,
+__device__ __noinline__ void compact_pull(const CP<OffT, EstT>& p_arg, uint32_t* qcnt, uint32_t* queue,
                              Shared& sh, RoundStat& st) {
+  const CP<OffT, EstT>& p = c_params<OffT, EstT>;  // constant bank, not p_arg
+  (void)p_arg;
   const uint32_t tid = threadIdx.x;
   unsigned long long evals = 0, escan = 0;
   for (int c = 0; c < NCLS; ++c) {
@@ -2193,7 +2237,22 @@ cudaError_t launch_t(const SolveBuffers& b, const SolveConfig& c, uint32_t r_beg
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   dim3 grid(c.num_sms), block(SOLVE_THREADS);
   void* args[] = {&p};
-  return cudaLaunchCooperativeKernel((const void*)kern, grid, block, args, smem, stream);
+  // c_params is one copy per device: order this solve's copy after the
+  // previous solve's kernel (whatever its stream) and publish our own end
+  static std::mutex mu;
+  static cudaEvent_t done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  cudaEvent_t& ev = done[dev & 63];
+  if (!ev && (e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(stream, ev, 0)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbolAsync(c_params<OffT, EstT>, &p, sizeof(p), 0, cudaMemcpyHostToDevice,
+                                   stream)) != cudaSuccess)
+    return e;
+  e = cudaLaunchCooperativeKernel((const void*)kern, grid, block, args, smem, stream);
+  if (e != cudaSuccess) return e;
+  return cudaEventRecord(ev, stream);
 }
 
 template <typename OffT, typename EstT>
