@@ -20,8 +20,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libkcore_b200.so")
-SOURCES = ["kc_solve.cu", "kc_count.cu", "kc_tail.cu", "kc_peel.cu", "kc_prep.cu", "kc_api.cu", "kc_gen.cu", "kc_ingest.cu", "kc_stage.cu"]
-HEADERS = ["kc_internal.h", "kc_dev.cuh", os.path.join("..", "..", "include", "kcore_b200.h")]
+SOURCES = ["kc_solve.cu", "kc_count.cu", "kc_count_split.cu", "kc_tail.cu", "kc_peel.cu", "kc_prep.cu", "kc_api.cu", "kc_gen.cu", "kc_ingest.cu", "kc_stage.cu"]
+HEADERS = ["kc_internal.h", "kc_dev.cuh", "kc_count_impl.cuh", os.path.join("..", "..", "include", "kcore_b200.h")]
 
 
 def nvcc() -> str:

@@ -317,7 +317,8 @@ kc_status ensure_solver(kc_graph* g, uint32_t max_rounds) {
   CK(dmalloc((void**)&b.ctl, 2 * sizeof(Ctl), g->stream));
   CK(dmalloc((void**)&b.anydrop, 4 * sizeof(uint32_t), g->stream));
   CK(dmalloc((void**)&b.stats, (size_t)STAT_SLOTS * sizeof(RoundStat), g->stream));
-  CK(dmalloc((void**)&b.status, 4 * sizeof(uint32_t), g->stream));
+  CK(dmalloc((void**)&b.status, ST_SLOTS * sizeof(uint32_t), g->stream));
+  CK(cudaMemsetAsync(b.status, 0, ST_SLOTS * sizeof(uint32_t), g->stream));
   CK(dmalloc((void**)&b.tailc, TAIL_SLOTS * sizeof(unsigned long long), g->stream));
   if (!g->d_out) CK(dmalloc((void**)&g->d_out, (g->n ? g->n : 1) * sizeof(uint32_t), g->stream));
   if (!g->d_k) CK(dmalloc((void**)&g->d_k, 2 * sizeof(unsigned long long), g->stream));
@@ -368,6 +369,11 @@ uint32_t cache_entries(const kc_graph* g, const kc_options& o) {
   return (uint32_t)want;
 }
 
+uint32_t env_u32(const char* name, uint32_t dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? (uint32_t)std::strtoul(v, nullptr, 10) : dflt;
+}
+
 // Run the solver to convergence (or one round when `one_round`), leaving the
 // estimates on the device.  Fills the counters of `st`.
 kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_t r_end,
@@ -385,6 +391,14 @@ kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_
   c.tail_threshold = tail_switch ? o.batch : 0u;
   c.num_sms = g->num_sms;
   c.pull = (o.reserved[0] & KC_DEBUG_NO_PULL) ? 0u : 1u;
+  // per-phase kernels for the large rounds (development switches)
+  static const uint32_t split_rounds = env_u32("KC_SPLIT_ROUNDS", 0u);
+  static const uint32_t split_min = env_u32("KC_SPLIT_MIN", 4096u);
+  static const uint32_t split_cache = env_u32("KC_SPLIT_CACHE", 1u);
+  c.split_rounds = split_rounds;
+  c.split_min = split_min;
+  c.split_cache = split_cache;
+  g->sb.prof_ctas = (uint32_t)g->num_sms;
   if (uses_count_kernel(o))
     CK(launch_count_rounds(g->sb, c, g->est16, g->lay.off64, r_begin, r_end, g->stream));
   else

@@ -384,30 +384,58 @@ __device__ __forceinline__ uint4 ld_ids4_rt(const uint32_t* p, bool ro) {
   return ro ? ld_ids4<true>(p, 0) : ld_ids4<false>(p, 0);
 }
 
+// KC_STREAM_K: entries per thread per step (8: two 128-bit id loads, 4: one);
+// KC_STREAM_PREFETCH: the next step's ids are loaded before this step's
+// gathers are consumed (8 more live registers).  The per-phase kernels
+// (kc_count_split.cu) trade both for resident warps.  The callback always
+// sees 8 slots; with K = 4 the upper four are never valid (compile-time
+// zero bits of `ok`, so their code folds away).
+#ifndef KC_STREAM_K
+#define KC_STREAM_K 8
+#endif
+#ifndef KC_STREAM_PREFETCH
+#define KC_STREAM_PREFETCH 1
+#endif
 template <int NT, typename EstT, typename F>
 __device__ __forceinline__ void stream_row_rt(const uint32_t* src, bool ro, const EstT* snap,
                                               uint32_t me, uint64_t ob, uint64_t oe,
                                               const EstT* s_cache, uint32_t cache_n, F&& f,
                                               uint32_t cut = 0xffffffffu, bool stop = false) {
-  constexpr uint32_t STEP = (uint32_t)NT * 8;
+  constexpr int K = KC_STREAM_K;
+  constexpr bool PF = KC_STREAM_PREFETCH != 0;
+  static_assert(K == 4 || K == 8, "one or two 128-bit id loads per step");
+  constexpr uint32_t STEP = (uint32_t)NT * K;
   const uint32_t* base = src + (ob & ~(uint64_t)3) + 4 * me;  // this thread's first granule
   const uint32_t head = (uint32_t)(ob & 3);   // masked entries before the row
   const uint32_t len = (uint32_t)(oe - ob);
   const uint32_t end = head + len;            // relative end
   const uint32_t l0 = 4 * me, l1 = 4 * me + 4 * NT;
   uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-  if (l0 < end) q0 = ld_ids4_rt(base, ro);
-  if (l1 < end) q1 = ld_ids4_rt(base + 4 * NT, ro);
+  if (PF) {
+    if (l0 < end) q0 = ld_ids4_rt(base, ro);
+    if (K == 8 && l1 < end) q1 = ld_ids4_rt(base + 4 * NT, ro);
+  }
   for (uint32_t a = 0; a < end; a += STEP) {
     uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
-    const uint32_t nb = a + STEP;
-    if (nb + l0 < end) n0 = ld_ids4_rt(base + nb, ro);
-    if (nb + l1 < end) n1 = ld_ids4_rt(base + nb + 4 * NT, ro);
+    if (PF) {
+      const uint32_t nb = a + STEP;
+      if (nb + l0 < end) n0 = ld_ids4_rt(base + nb, ro);
+      if (K == 8 && nb + l1 < end) n1 = ld_ids4_rt(base + nb + 4 * NT, ro);
+    } else {
+      q0 = q1 = make_uint4(0, 0, 0, 0);
+      if (a + l0 < end) q0 = ld_ids4_rt(base + a, ro);
+      if (K == 8 && a + l1 < end) q1 = ld_ids4_rt(base + a + 4 * NT, ro);
+    }
     uint32_t ids[8], x[8];
     uint32_t ok = 0;
     bool past = false;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
+      if (k >= K) {
+        ids[k] = 0;
+        x[k] = 0;
+        continue;
+      }
       const uint32_t pos = a + (k < 4 ? l0 : l1) + (k & 3);
       ids[k] = u4_get(k < 4 ? q0 : q1, k & 3);
       const bool in = pos - head < len;  // head <= pos < end
@@ -418,8 +446,10 @@ __device__ __forceinline__ void stream_row_rt(const uint32_t* src, bool ro, cons
     }
     f(ok, ids, x);
     if (stop && __any_sync(FULL, past)) break;
-    q0 = n0;
-    q1 = n1;
+    if (PF) {
+      q0 = n0;
+      q1 = n1;
+    }
   }
 }
 

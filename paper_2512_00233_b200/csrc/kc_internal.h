@@ -82,13 +82,18 @@ struct SolveBuffers {
   RoundStat* stats;          // [STAT_SLOTS]
   uint32_t* status;          // [0] rounds completed, [1] converged, [2] stopped for the tail,
                              // [3] est buffer holding the current state
-  unsigned long long* prof;  // optional phase timestamps [PROF_ROUNDS][grid][PROF_PHASES]
+  unsigned long long* prof;  // optional phase timestamps [PROF_ROUNDS][prof_ctas][PROF_PHASES]
+  uint32_t prof_ctas;        // CTAs per profile row (the SM count)
   unsigned long long* tailc; // hybrid tail (kc_tail.cu): counters [TAIL_SLOTS]
 };
 // kc_tail.cu counters (tailc[]): pops (tail_pops), evaluations, notifications,
 // drops, adjacency entries scanned, "the tail ran"; slot 6 is scratch.
 enum TailSlot : int { TAIL_POPS = 0, TAIL_EVALS, TAIL_FIRES, TAIL_DROPS, TAIL_ESCAN, TAIL_RAN,
                       TAIL_SCRATCH, TAIL_SLOTS = 8 };
+// status[] slots; ST_HANDOFF: the per-phase kernels (kc_count_split.cu) met a small round and
+// left the rest to the persistent kernel
+enum StatusSlot : int { ST_ROUNDS = 0, ST_CONVERGED = 1, ST_TAIL = 2, ST_BUF = 3, ST_HANDOFF = 4,
+                        ST_SLOTS = 8 };
 constexpr uint32_t PROF_ROUNDS = 256;
 constexpr uint32_t PROF_PHASES = 8;
 
@@ -103,6 +108,10 @@ struct SolveConfig {
   int num_sms;
   uint32_t pull;             // counting rule: round 0's notify + round 1's evaluate as one
                              // pull phase (kc_count.cu PULL) when the launch covers rounds 0-1
+  uint32_t split_rounds;     // counting rule, whole solves: rounds 1 .. split_rounds run one
+                             // kernel per phase (kc_count_split.cu) while they start with at
+  uint32_t split_min;        // least split_min active vertices (0 rounds: off)
+  uint32_t split_cache;      // the per-phase kernels keep the shared-memory estimate cache
 };
 
 // Launch rounds [r_begin, r_end) of the persistent solver on `stream`.
@@ -112,6 +121,11 @@ cudaError_t launch_rounds(const SolveBuffers& b, const SolveConfig& c, bool est1
 // The counting-rule solver (kc_count.cu): same contract.
 cudaError_t launch_count_rounds(const SolveBuffers& b, const SolveConfig& c, bool est16, bool off64,
                                 uint32_t r_begin, uint32_t r_end, cudaStream_t stream);
+// Rounds [r_lo, r_hi] one kernel per phase (kc_count_split.cu), queued without host round
+// trips; they return at once after convergence or the hand-off (ST_HANDOFF).
+cudaError_t launch_count_phases(const SolveBuffers& b, const SolveConfig& c, bool est16, bool off64,
+                                uint32_t r_lo, uint32_t r_hi, bool skip_first_eval,
+                                cudaStream_t stream);
 // FastK's sequential tail (fastk.cpp:28-55) on one CTA, after the rounds
 // kernel stopped for it (status[2] == 1) — or, with force_flags >= 0, from
 // the active set in flag[force_flags] (observed mode).  No-op otherwise.
