@@ -136,9 +136,9 @@ kc_status kc_graph_upload_device(const kc_csr_view* csr, int device, kc_graph** 
 #define KC_UPLOAD_FORCE_OFF64 1u /* 64-bit device offsets even when nnz < 2^32 */
 #define KC_UPLOAD_FORCE_EST32 2u /* 32-bit estimates even when H < 2^15 */
 #define KC_UPLOAD_UNSORTED_ROWS 4u /* keep relabelled rows in input order: skips the
-                                      per-row sort (~10 ms on R-MAT 22) at 13-75% slower
-                                      solves (no sorted-row degree cuts) — for one-shot
-                                      solves (kc_fastk_run) */
+                                      on-chip row sorts of the layout (A/B and tests;
+                                      solves are 20-30% slower without the sorted-row
+                                      degree cuts) */
 kc_status kc_graph_upload_ex(const kc_csr_view* csr, int device, int on_device, uint32_t flags,
                              kc_graph** out);
 void kc_graph_free(kc_graph* g);
@@ -200,8 +200,9 @@ kc_status kc_verify(kc_graph* g, const kc_options* opt, kc_mismatch* out, uint64
 kc_status kc_sequential_tail(kc_graph* g, uint32_t* est, uint8_t* active, int extended_notify,
                              kc_stats* stats);
 
-/* One-shot drop-in: upload (KC_UPLOAD_UNSORTED_ROWS) + solve + download + free
- * (fastk_run semantics). */
+/* One-shot drop-in: upload (sorted layout, rows sorted while each chunk of the
+ * host-to-device copy is relabelled) + solve + download + free (fastk_run
+ * semantics). */
 kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* coreness,
                        kc_stats* stats);
 
@@ -225,6 +226,13 @@ kc_status kc_debug_round_stats(kc_graph* g, unsigned long long* out, uint32_t ro
  * alone over every adjacency entry — the id stream plus one estimate gather
  * each, no cache — after a solve; *ms_per_pass = device time per pass. */
 kc_status kc_debug_gather_probe(kc_graph* g, int reps, float* ms_per_pass);
+/* Debug: the handle's on-device layout copied to HOST arrays — offsets
+ * [n_nz + 1] (widened to 64 bit), neighbours [nnz] in the relabelled ids, and
+ * perm [n] (new id -> caller id).  *n_nz receives the number of non-isolated
+ * vertices, *rows_sorted whether every row is ascending.  Any output may be
+ * NULL.  For layout tests. */
+kc_status kc_debug_layout(kc_graph* g, uint64_t* offsets, uint32_t* neighbors, uint32_t* perm,
+                          uint32_t* n_nz, int* rows_sorted);
 
 /* ---- synthetic inputs (BASELINE.json configs; the "kcgen v1" spec) ------ */
 /* Build one of the five configs (1..5) — or a scaled variant — directly on

@@ -71,6 +71,7 @@ ABI_SYMBOLS = (
     "kc_csr_dev_free", "kc_csr_dev_download", "kc_debug_phase_times", "kc_graph_upload_ex",
     "kc_debug_round_stats", "kc_debug_gather_probe", "kc_solve_traced", "kc_peel", "kc_verify", "kc_load_edge_list",
     "kc_load_edge_list_file", "kc_csr_dev_original_ids", "kc_sequential_tail",
+    "kc_debug_layout",
 )
 KC_DEBUG_PHASE_TIMES = 1
 KC_DEBUG_LEGACY_COUNT = 2
@@ -158,6 +159,9 @@ def load_library():
     L.kc_debug_round_stats.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32]
     L.kc_debug_gather_probe.restype = C.c_int
     L.kc_debug_gather_probe.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_float)]
+    L.kc_debug_layout.restype = C.c_int
+    L.kc_debug_layout.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.POINTER(C.c_uint32), C.POINTER(C.c_int)]
     L.kc_csr_dev_download.restype = C.c_int
     L.kc_csr_dev_download.argtypes = [C.POINTER(_CSRDev), C.c_void_p, C.c_void_p]
     _lib = L
@@ -573,6 +577,20 @@ class GpuGraph:
         _check(load_library().kc_debug_gather_probe(self._h, reps, C.byref(ms)),
                "kc_debug_gather_probe")
         return ms.value
+
+    def layout(self):
+        """(offsets [n_nz + 1], neighbours [nnz], perm [n], rows_sorted): the
+        handle's relabelled CSR on the host (debug; kc_debug_layout)."""
+        L = load_library()
+        n_nz, srt = C.c_uint32(), C.c_int()
+        _check(L.kc_debug_layout(self._h, None, None, None, C.byref(n_nz), C.byref(srt)),
+               "kc_debug_layout")
+        off = np.zeros(n_nz.value + 1, dtype=np.uint64)
+        adj = np.zeros(max(int(L.kc_graph_nnz(self._h)), 1), dtype=np.uint32)
+        perm = np.zeros(max(int(L.kc_graph_n(self._h)), 1), dtype=np.uint32)
+        _check(L.kc_debug_layout(self._h, off.ctypes.data, adj.ctypes.data, perm.ctypes.data,
+                                 None, None), "kc_debug_layout")
+        return off, adj[: int(L.kc_graph_nnz(self._h))], perm[: int(L.kc_graph_n(self._h))], bool(srt.value)
 
     def round_stats(self, rounds: int) -> np.ndarray:
         """[rounds, 9] per-round counters of the last solve (debug): evals,

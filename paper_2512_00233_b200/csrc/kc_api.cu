@@ -573,8 +573,17 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
     uint64_t k = (bytes + (64ull << 20) - 1) / (64ull << 20);
     k = k < 1 ? 1 : k > 16 ? 16 : k;
     old_lo.push_back(0);
-    for (uint64_t c = 1; c < k; ++c) {  // first row whose start is >= c/k of the entries
-      const uint64_t target = g->nnz * c / k;
+    // cut points in 1/(4k) of the entries: k equal chunks; when a chunk is
+    // large (>= 256 MB) the last one is cut again into 1/2, 1/4, 1/4 — only the
+    // last chunk's layout is not hidden under a copy
+    std::vector<uint64_t> cuts;
+    for (uint64_t c = 1; c < k; ++c) cuts.push_back(4 * c);
+    if (bytes / k >= (256ull << 20)) {
+      cuts.push_back(4 * k - 2);
+      cuts.push_back(4 * k - 1);
+    }
+    for (uint64_t q : cuts) {  // first row whose start is >= q/(4k) of the entries
+      const uint64_t target = (uint64_t)((unsigned __int128)g->nnz * q / (4 * k));
       uint32_t lo = old_lo.back(), hi = g->n;
       while (lo < hi) {
         const uint32_t mid = lo + (hi - lo) / 2;
@@ -1065,6 +1074,31 @@ kc_status kc_debug_gather_probe(kc_graph* g, int reps, float* ms_per_pass) {
   return KC_OK;
 }
 
+kc_status kc_debug_layout(kc_graph* g, uint64_t* offsets, uint32_t* neighbors, uint32_t* perm,
+                          uint32_t* n_nz, int* rows_sorted) {
+  kcb::DeviceGuard device_guard;
+  if (!g) return fail(KC_ERR_INVALID_ARGUMENT, "null argument");
+  CK(cudaSetDevice(g->device));
+  if (n_nz) *n_nz = g->n ? g->lay.n_nz : 0u;
+  if (rows_sorted) *rows_sorted = g->n && g->lay.rows_sorted ? 1 : 0;
+  if (g->n == 0) return KC_OK;
+  CK(cudaStreamSynchronize(g->stream));
+  const size_t m = (size_t)g->lay.n_nz + 1;
+  if (offsets) {
+    if (g->lay.off64) {
+      CK(cudaMemcpy(offsets, g->lay.off, m * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    } else {
+      std::vector<uint32_t> tmp(m);
+      CK(cudaMemcpy(tmp.data(), g->lay.off, m * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < m; ++i) offsets[i] = tmp[i];
+    }
+  }
+  if (neighbors && g->nnz)
+    CK(cudaMemcpy(neighbors, g->lay.adj, g->nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  if (perm) CK(cudaMemcpy(perm, g->lay.perm, (size_t)g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return KC_OK;
+}
+
 static kc_status ensure_peel(kc_graph* g) {
   if (g->peel_ready) return KC_OK;
   const size_t m = (size_t)g->lay.n_nz + 1;
@@ -1295,7 +1329,7 @@ kc_status kc_verify(kc_graph* g, const kc_options* opt, kc_mismatch* out, uint64
 }
 
 #ifndef KC_ONESHOT_SORT
-#define KC_ONESHOT_SORT 0
+#define KC_ONESHOT_SORT 1  // 0: keep the relabelled rows in input order (A/B)
 #endif
 kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* coreness,
                        kc_stats* st) {
@@ -1303,7 +1337,8 @@ kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* 
   kc_status s = validate(opt, &o);  // invalid options rejected before any work
   if (s != KC_OK) return s;
   kc_graph* g = nullptr;
-  // one solve: the per-row sort of the layout would cost more than it saves
+  // sorted layout: the rows are sorted on chip while each upload chunk is
+  // relabelled (kc_prep.cu), under the copy of the next chunk
   s = kc_graph_upload_ex(csr, 0, 0, KC_ONESHOT_SORT ? 0u : KC_UPLOAD_UNSORTED_ROWS, &g);
   if (s != KC_OK) return s;
   s = kc_solve(g, &o, coreness, st);
