@@ -17,6 +17,7 @@
 #include <cstring>
 #include <functional>
 #include <mutex>
+#include <cstdlib>
 #include <thread>
 #include <vector>
 
@@ -33,7 +34,11 @@ class CopyPool {
  public:
   CopyPool() {
     unsigned hc = std::thread::hardware_concurrency();
-    nthreads_ = std::max(1u, std::min(8u, hc ? hc / 2 : 4u));
+    // measured on the 16-core B200 host (scripts/stage_ab.sh): R-MAT 26's 8.95 GB stage in
+    // 333 / 275 / 221 / 200 ms with 4 / 8 / 12 / 16 threads (R-MAT 22: 19.7 / 15.6 / 16.3 / 16.3)
+    nthreads_ = std::max(1u, std::min(16u, hc ? hc : 4u));
+    if (const char* v = std::getenv("KC_STAGE_THREADS"))  // development override
+      if (*v) nthreads_ = std::max(1u, std::min(64u, (unsigned)std::strtoul(v, nullptr, 10)));
     for (unsigned i = 1; i < nthreads_; ++i) workers_.emplace_back([this, i] { loop(i); });
   }
   ~CopyPool() {
