@@ -682,6 +682,8 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
   uint32_t* tiers = nullptr;
   uint32_t *tier_list = nullptr, *tier_cnt = nullptr;
   void* hub_tmp_store = nullptr;
+  cudaStream_t hs = nullptr;  // sorted layouts: the hubs' relabel + sort, beside the tiers
+  cudaEvent_t hev = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0, need = 0;
   uint32_t hb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -843,6 +845,12 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
                                                         (int)n_huge, sb, se, 0, end_bit, s));
       }
       PREP_CK(dmalloc(&hub_tmp_store, hub_tmp_bytes ? hub_tmp_bytes : 1, s));
+      // the hubs of a chunk are sorted one CTA each (a 500 K-entry hub takes
+      // ~1 ms alone): on their own stream they run beside the tier kernels
+      PREP_CK(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking));
+      PREP_CK(cudaEventCreateWithFlags(&hev, cudaEventDisableTiming));
+      PREP_CK(cudaEventRecord(hev, s));  // allocations and tables above are stream-ordered on s
+      PREP_CK(cudaStreamWaitEvent(hs, hev, 0));
     }
     // relabel: all rows at once, or — pipelined upload — the rows of each
     // chunk of old ids as soon as its bytes have landed (event), so the
@@ -877,12 +885,14 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
       }
       if (n_big) {
         uint32_t* dst = fused_sort ? hub_buf[0] : new_adj;
+        cudaStream_t rs = fused_sort ? hs : s;
+        if (fused_sort && feed) PREP_CK(cudaStreamWaitEvent(hs, feed->ready[c], 0));
         if (off64)
-          relabel_rows_kernel<uint64_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_big,
+          relabel_rows_kernel<uint64_t><<<G, B, 0, rs>>>(off, adj, perm, inv, chunks, n_big,
                                                         (const uint64_t*)new_off, dst, total,
                                                         o_lo, o_hi, n, bounds + 7);
         else
-          relabel_rows_kernel<uint32_t><<<G, B, 0, s>>>(off, adj, perm, inv, chunks, n_big,
+          relabel_rows_kernel<uint32_t><<<G, B, 0, rs>>>(off, adj, perm, inv, chunks, n_big,
                                                         (const uint32_t*)new_off, dst, total,
                                                         o_lo, o_hi, n, bounds + 7);
         PREP_CK(cudaGetLastError());
@@ -896,7 +906,7 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
             cub::TransformInputIterator<int, SegEnd<uint64_t>, cub::CountingInputIterator<int>> se(
                 cub::CountingInputIterator<int>(0), SegEnd<uint64_t>{o, perm, o_lo, o_hi});
             PREP_CK(cub::DeviceSegmentedRadixSort::SortKeys(hub_tmp_store, nb, db, (int)hub_entries,
-                                                            (int)n_huge, sb, se, 0, end_bit, s));
+                                                            (int)n_huge, sb, se, 0, end_bit, hs));
           } else {
             const uint32_t* o = (const uint32_t*)new_off;
             cub::TransformInputIterator<int, SegBegin<uint32_t>, cub::CountingInputIterator<int>> sb(
@@ -904,7 +914,7 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
             cub::TransformInputIterator<int, SegEnd<uint32_t>, cub::CountingInputIterator<int>> se(
                 cub::CountingInputIterator<int>(0), SegEnd<uint32_t>{o, perm, o_lo, o_hi});
             PREP_CK(cub::DeviceSegmentedRadixSort::SortKeys(hub_tmp_store, nb, db, (int)hub_entries,
-                                                            (int)n_huge, sb, se, 0, end_bit, s));
+                                                            (int)n_huge, sb, se, 0, end_bit, hs));
           }
           if (!hub_roles_known) {
             hub_roles_known = true;
@@ -913,13 +923,17 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
               // (the other rows are rewritten by their own chunks) and let the
               // later chunks start from new_adj, so they end in new_adj
               PREP_CK(cudaMemcpyAsync(new_adj, db.Current(), (size_t)hub_entries * sizeof(uint32_t),
-                                      cudaMemcpyDeviceToDevice, s));
+                                      cudaMemcpyDeviceToDevice, hs));
               hub_buf[0] = new_adj;
               hub_buf[1] = sort_tmp;
             }
           }
         }
       }
+    }
+    if (hs) {  // the layout is complete when both streams are
+      PREP_CK(cudaEventRecord(hev, hs));
+      PREP_CK(cudaStreamWaitEvent(s, hev, 0));
     }
     {
       if (fused_sort) out->rows_sorted = true;
@@ -944,6 +958,11 @@ cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, ui
   new_adj = nullptr;
   perm = nullptr;
 done:
+  if (hs) {
+    cudaStreamSynchronize(hs);
+    cudaStreamDestroy(hs);
+  }
+  if (hev) cudaEventDestroy(hev);
   dfree(deg, s);
   dfree(iota, s);
   dfree(sdeg, s);
