@@ -369,6 +369,13 @@ uint32_t cache_entries(const kc_graph* g, const kc_options& o) {
   return (uint32_t)want;
 }
 
+#ifndef KC_SPLIT_ROUNDS_DEFAULT
+#define KC_SPLIT_ROUNDS_DEFAULT 16u   // rounds 1 .. 16 one kernel per phase while they are large
+#endif                                // (24 from 1e9 entries: the rounds stay large longer; a
+                                      // launch after the hand-off is a ~4 us no-op)
+#ifndef KC_SPLIT_MIN_BIG_ROWS
+#define KC_SPLIT_MIN_BIG_ROWS 65536u  // ... on graphs with at least this many rows of degree > 64
+#endif
 uint32_t env_u32(const char* name, uint32_t dflt) {
   const char* v = std::getenv(name);
   return v && *v ? (uint32_t)std::strtoul(v, nullptr, 10) : dflt;
@@ -391,11 +398,20 @@ kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_
   c.tail_threshold = tail_switch ? o.batch : 0u;
   c.num_sms = g->num_sms;
   c.pull = (o.reserved[0] & KC_DEBUG_NO_PULL) ? 0u : 1u;
-  // per-phase kernels for the large rounds (development switches)
-  static const uint32_t split_rounds = env_u32("KC_SPLIT_ROUNDS", 0u);
-  static const uint32_t split_min = env_u32("KC_SPLIT_MIN", 4096u);
+  // Per-phase kernels (kc_count_split.cu) for the large rounds of a whole
+  // solve: on by default for graphs with enough vertices of degree > 64 (the
+  // warp / CTA list scans they speed up); each of their launches costs ~4 us,
+  // which small graphs do not earn back (ER: 0.52 -> 0.79 ms with them).
+  // KC_SPLIT_ROUNDS (0: off) / KC_SPLIT_MIN / KC_SPLIT_CACHE override.
+  static const char* split_env = std::getenv("KC_SPLIT_ROUNDS");
+  static const uint32_t split_rounds_env = env_u32("KC_SPLIT_ROUNDS", 0u);
+  const uint32_t split_rounds = (split_env && *split_env) ? split_rounds_env
+                                : g->nnz >= 1000000000ull ? KC_SPLIT_ROUNDS_DEFAULT + 8u
+                                                          : KC_SPLIT_ROUNDS_DEFAULT;
+  static const uint32_t split_min = env_u32("KC_SPLIT_MIN", 1024u);
   static const uint32_t split_cache = env_u32("KC_SPLIT_CACHE", 1u);
-  c.split_rounds = split_rounds;
+  const bool split_fits = g->lay.cls_begin[C_SUB] >= KC_SPLIT_MIN_BIG_ROWS;
+  c.split_rounds = (split_env && *split_env) || split_fits ? split_rounds : 0u;
   c.split_min = split_min;
   c.split_cache = split_cache;
   g->sb.prof_ctas = (uint32_t)g->num_sms;

@@ -201,7 +201,7 @@ struct CP {
 };
 constexpr uint32_t R_RESUME = 0xffffffffu;  // r_begin: carry on at round status[0]
 #ifndef KC_SPLIT_CTAS
-#define KC_SPLIT_CTAS 2            // per-phase kernels: CTAs per SM (kc_count_split.cu)
+#define KC_SPLIT_CTAS 1            // per-phase kernels: CTAs per SM (kc_count_split.cu)
 #endif
 
 // The solver's parameters in constant memory, for the out-of-line phase
