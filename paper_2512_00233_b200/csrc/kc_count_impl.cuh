@@ -100,6 +100,17 @@ constexpr uint32_t LIST_MIN_DEG = KC_LIST_MIN_DEG;  // rows longer than this kee
 #define KC_WARP_MAX_LEN DEG_BIG_MAX
 #endif
 constexpr uint32_t WARP_MAX_LEN = KC_WARP_MAX_LEN;  // longest scan a single warp takes
+// ... in a small round (fewer than WML_SMALL_ACTIVE active vertices) only
+// WML_SMALL: most warps are idle there and a hub's 8 K-entry list on one warp
+// is the round's critical path (64 dependent steps); CTA-wide it is 3.
+// Chung-Lu's rounds 10-72 (0.5-2 K hubs, nothing else): 13.0 -> 11.9 ms.
+#ifndef KC_WML_SMALL
+#define KC_WML_SMALL 2048
+#endif
+#ifndef KC_WML_SMALL_ACTIVE
+#define KC_WML_SMALL_ACTIVE 8192
+#endif
+constexpr uint32_t WML_SMALL = KC_WML_SMALL, WML_SMALL_ACTIVE = KC_WML_SMALL_ACTIVE;
 constexpr int HREG = HIST_BINS > (int)NWARPS * WARP_BINS ? HIST_BINS : (int)NWARPS * WARP_BINS;
 #ifndef KC_WQ
 #define KC_WQ 64
@@ -227,6 +238,7 @@ struct View {
   bool r0;
   bool pull;             // the PULL phase: every vertex evaluated against N
   uint32_t round;
+  uint32_t wml;          // longest hub scan a single warp takes this round (see WML_SMALL)
 };
 
 struct Acc {  // per-thread counters, flushed per round
@@ -1883,7 +1895,7 @@ __device__ __forceinline__ void eval_phase(const CP<OffT, EstT>& p, const View<E
   huge_warps(p, v, sh, ctl, ph, [&](uint32_t u) {
     const Item it = eval_item<PULL>(p, v, s_cache, u);  // metadata loaded once
     // (round 0 on sorted rows reads a prefix only: always a warp's)
-    if (it.len > WARP_MAX_LEN && !(KC_R0_SORTED && v.r0 && p.dc.sorted)) return false;
+    if (it.len > v.wml && !(KC_R0_SORTED && v.r0 && p.dc.sorted)) return false;
     eval_warp<PULL>(p, v, s_cache, w_bins, it, acc);
     return true;
   });
@@ -2007,7 +2019,7 @@ __device__ __forceinline__ void notify_phase(const CP<OffT, EstT>& p, const View
   huge_warps(p, v, sh, ctl, 1, [&](uint32_t u) {
     const Drop d = drop_item(p, u);  // metadata loaded once
     if (d.t >= d.cap) return true;   // round 0: evaluated, no drop
-    if (d.len > WARP_MAX_LEN) return false;
+    if (d.len > v.wml) return false;
     acc.fires += notify_drop_warp(p, q, s_cache, cache_n, w_bins, r, d);
     if (lane_id() == 0) acc.nscan += d.len;
     return true;
@@ -2104,6 +2116,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     vl.r0 = r == 0;
     vl.pull = false;
     vl.round = r;
+    vl.wml = WARP_MAX_LEN;
     unsigned long long* pf = (p.prof && r < PROF_ROUNDS && tid == 0)
                                  ? p.prof + ((size_t)r * gridDim.x + blockIdx.x) * PROF_PHASES
                                  : nullptr;
@@ -2125,6 +2138,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     if (tid == 0) sh.drop = 0;
     const uint32_t cache_n = active >= CACHE_MIN_ACTIVE ? p.cache_n : 0u;
     vl.cache_n = cache_n;
+    if (r > 0 && active < WML_SMALL_ACTIVE) vl.wml = WML_SMALL;
     if (cache_n && !evaluated) fill_cache(s_cache, (const EstT*)p.E, cache_n);
     if (tid == 0) s_view = vl;
     __syncthreads();
@@ -2271,6 +2285,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, KC_SPLIT_CTAS)
   vl.r0 = false;
   vl.pull = false;
   vl.round = r;
+  vl.wml = active < WML_SMALL_ACTIVE ? WML_SMALL : WARP_MAX_LEN;
   const uint32_t cache_n = active >= CACHE_MIN_ACTIVE ? p.cache_n : 0u;
   vl.cache_n = cache_n;
   Ctl& ctl = p.ctl[cur];
