@@ -20,7 +20,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libkcore_b200.so")
-SOURCES = ["kc_solve.cu", "kc_count.cu", "kc_count_split.cu", "kc_tail.cu", "kc_peel.cu", "kc_prep.cu", "kc_api.cu", "kc_gen.cu", "kc_ingest.cu", "kc_stage.cu"]
+SOURCES = ["kc_solve.cu", "kc_count.cu", "kc_count_split.cu", "kc_tail.cu", "kc_peel.cu", "kc_prep.cu", "kc_api.cu", "kc_gen.cu", "kc_ingest.cu", "kc_stage.cu", "kc_hostcopy.cpp"]
 HEADERS = ["kc_internal.h", "kc_dev.cuh", "kc_count_impl.cuh", os.path.join("..", "..", "include", "kcore_b200.h")]
 
 
@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(build_dir, src.replace(".cu", ".o"))
+        o = os.path.join(build_dir, os.path.splitext(src)[0] + ".o")
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
             jobs.append([nvcc()] + FLAGS + [f"-D{d}" for d in defines] + ["-c", s, "-o", o])

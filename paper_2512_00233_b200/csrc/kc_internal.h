@@ -220,6 +220,7 @@ struct AdjFeed {
 // Pageable host memory (kc_stage.cu): copies through pinned staging slots
 // filled by host threads while the copy engine drains the previous slot.
 bool is_pageable(const void* p);
+void host_copy(void* dst, const void* src, size_t n);  // kc_hostcopy.cpp: non-temporal stores
 cudaError_t staged_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
 cudaError_t staged_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 cudaError_t prep_layout(const uint64_t* off, const uint32_t* adj, uint32_t n, uint64_t nnz,

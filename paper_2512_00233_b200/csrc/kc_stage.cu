@@ -53,7 +53,7 @@ class CopyPool {
   // dst[0, n) = src[0, n), split over the pool (the caller takes part 0)
   void copy(void* dst, const void* src, size_t n) {
     if (n < (1u << 20) || nthreads_ == 1) {
-      std::memcpy(dst, src, n);
+      host_copy(dst, src, n);
       return;
     }
     {
@@ -74,7 +74,7 @@ class CopyPool {
   void part(unsigned i) {
     const size_t per = (n_ + nthreads_ - 1) / nthreads_;
     const size_t a = std::min(n_, per * i), b = std::min(n_, a + per);
-    if (b > a) std::memcpy(dst_ + a, src_ + a, b - a);
+    if (b > a) host_copy(dst_ + a, src_ + a, b - a);
   }
   void loop(unsigned i) {
     uint64_t seen = 0;
