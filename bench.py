@@ -273,7 +273,10 @@ def roofline(m, rule):
     gather_rate = m["nnz"] / (m["probe_ms"] * 1e-3)
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": profile_traffic(m["cfg"], kname),
-            "peak_source": peak_src, "kernel": f"{kname} (persistent)",
+            "peak_source": peak_src,
+            "kernel": (f"{kname} (persistent: round 0 + PULL, small rounds) + count_phase_kernel<0|1> "
+                       "(one per phase of the large rounds), whole solve" if kname == "count_rounds_kernel"
+                       and int(m["st"].get("kernel_launches", 0)) > 6 else f"{kname} (persistent)"),
             "bytes_alg_per_launch": bytes_alg,
             "gather_ceiling": {
                 "what": "kc_debug_gather_probe: id stream + one estimate gather per adjacency "

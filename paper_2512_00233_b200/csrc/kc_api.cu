@@ -208,6 +208,7 @@ struct kc_graph {
   unsigned long long* d_prof = nullptr;  // phase timestamps (debug)
   unsigned long long* d_count = nullptr; // observed mode: active-flag count
   uint32_t state_buf = 0;                // est buffer holding the current state
+  uint32_t round_launches = 1;           // solver kernels queued by the last run_rounds
   unsigned long long* d_k = nullptr;
   // independent peel / verify (allocated at first use)
   bool peel_ready = false;
@@ -415,6 +416,11 @@ kc_status run_rounds(kc_graph* g, const kc_options& o, uint32_t r_begin, uint32_
   c.split_min = split_min;
   c.split_cache = split_cache;
   g->sb.prof_ctas = (uint32_t)g->num_sms;
+  // solver kernels this call queues (kc_stats.kernel_launches): the persistent kernel, or
+  // persistent + 2 per per-phase round + persistent again (launch_count_rounds)
+  g->round_launches = 1u;
+  if (uses_count_kernel(o) && c.split_rounds && r_begin == 0 && r_end > 2)
+    g->round_launches = 2u + 2u * (c.split_rounds < r_end - 1 ? c.split_rounds : r_end - 1);
   if (uses_count_kernel(o))
     CK(launch_count_rounds(g->sb, c, g->est16, g->lay.off64, r_begin, r_end, g->stream));
   else
@@ -853,8 +859,8 @@ static kc_status solve_impl(kc_graph* g, const kc_options* opt, uint32_t* out, b
   CK(cudaStreamSynchronize(g->stream));
   hc.mark("solve: done");
   if (st) {
-    // init + rounds (+ tail list + tail) + k stats + permute-back
-    st->kernel_launches = 2u + (uses_tail(o) ? 2u : 0u) + 2u;
+    // init + solver kernels (+ tail list + tail) + k stats + permute-back
+    st->kernel_launches = 1u + g->round_launches + (uses_tail(o) ? 2u : 0u) + 2u;
     cudaEventElapsedTime(&st->t_solve_ms, g->ev[0], g->ev[1]);
     cudaEventElapsedTime(&st->t_download_ms, g->ev[2], g->ev[3]);
   }

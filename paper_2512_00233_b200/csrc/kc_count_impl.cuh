@@ -241,8 +241,10 @@ struct View {
   uint32_t wml;          // longest hub scan a single warp takes this round (see WML_SMALL)
 };
 
-struct Acc {  // per-thread counters, flushed per round
-  unsigned long long evals, escan, drops, fires, nscan, ascan;
+struct Acc {  // per-thread counters of one round (one phase in the per-phase kernels), flushed
+              // into 64-bit sums per round; 32 bits each: a thread's own share of a round's
+              // entries (six registers less than 64-bit counters, live through the whole kernel)
+  uint32_t evals, escan, drops, fires, nscan, ascan;
   bool any_drop;
 };
 
@@ -1561,7 +1563,7 @@ __device__ __forceinline__ void notify_wclass_impl(const CP<OffT, EstT>& p, cons
   const uint32_t cache_n = v.cache_n;
   const bool r0 = v.r0;
   uint32_t fires = 0;
-  unsigned long long nscan = 0;
+  uint32_t nscan = 0;
   for_class(p, v, c, gmax, [&](uint32_t u, uint32_t n) {
     Drop mine{};
     if (lane_id() < n) {
