@@ -17,6 +17,8 @@
 #include <thread>
 #include <new>
 #include <string>
+#include <atomic>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/kcore_b200.h"
@@ -31,11 +33,60 @@ thread_local std::string g_last_error;
 }  // namespace
 
 namespace kcb {
+static cudaMemPool_t g_pools[64];
+void pool_debug(const char* what) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool = g_pools[dev & 63];
+  if (!pool) return;
+  uint64_t res = 0, used = 0, hi = 0;
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &hi);
+  std::fprintf(stderr, "[kc host] pool %-12s reserved %.1f MB used %.1f MB high %.1f MB\n", what,
+               res / 1e6, used / 1e6, hi / 1e6);
+}
+// Large blocks are recycled by exact size in front of the pool.  The pool
+// keeps its memory (release threshold), but when the sizes are not page
+// multiples (n = 20,000,000: 80,000,000-byte arrays, 1,557,878,200-byte
+// adjacency) it re-maps the reserved pages into a fresh address range on
+// every call: 0.6 ms per 80 MB, 6-10 ms per 1.5 GB — 22 ms of a 64 ms
+// one-shot solve of the Chung-Lu graph, none on the power-of-two R-MAT sizes.
+// A one-shot solve of the same graph size asks for the same sizes in the same
+// order, so every request finds the block the previous call returned.  A
+// returned block carries an event recorded on the stream that freed it and
+// the next owner's stream waits on it (stream-ordered like cudaFreeAsync).
+// Blocks not asked for during two consecutive uploads (another graph size)
+// go back to the pool at the next miss, and all of them do when the pool
+// runs out of memory.
+namespace blockcache {
+constexpr size_t CACHE_MIN_BYTES = 1u << 20;
+struct IdleBlock {
+  void* p;
+  cudaEvent_t ev;
+  uint64_t gen;  // upload generation it was returned in
+};
+struct BlockCache {
+  std::mutex m;
+  std::unordered_map<void*, size_t> live;              // handed out: pointer -> bytes
+  std::unordered_multimap<size_t, IdleBlock> idle;     // returned, by exact size
+};
+BlockCache g_cache[64];
+std::atomic<uint64_t> g_gen{2};  // bumped per uploaded handle (upload_common)
+bool cache_on() {
+  static const bool on = [] {
+    const char* v = std::getenv("KC_BLOCK_CACHE");
+    return !(v && *v == '0');
+  }();
+  return on;
+}
+}  // namespace blockcache
+using namespace blockcache;
+
 cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t s) {
   // the library's own pool per device (not the device's default pool: its
   // release threshold is process-wide state other libraries rely on)
   static std::once_flag once[64];
-  static cudaMemPool_t pools[64];
   int dev = 0;
   cudaGetDevice(&dev);
   std::call_once(once[dev & 63], [dev] {
@@ -48,17 +99,74 @@ cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t s) {
     if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
       uint64_t keep = UINT64_MAX;  // keep freed blocks for the next solve
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      pools[dev & 63] = pool;
+      g_pools[dev & 63] = pool;
     } else {
       cudaGetLastError();
-      pools[dev & 63] = nullptr;  // fall back to the default pool, untouched
+      g_pools[dev & 63] = nullptr;  // fall back to the default pool, untouched
     }
   });
   static const bool dbg = std::getenv("KC_DEBUG_HOST") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
-  cudaMemPool_t pool = pools[dev & 63];
-  const cudaError_t e = pool ? cudaMallocFromPoolAsync(p, bytes ? bytes : 1, pool, s)
-                             : cudaMallocAsync(p, bytes ? bytes : 1, s);
+  if (!bytes) bytes = 1;
+  BlockCache& bc = g_cache[dev & 63];
+  const bool big = bytes >= CACHE_MIN_BYTES && cache_on();
+  auto release = [s](const std::vector<IdleBlock>& v) {  // back to the pool, after their last use
+    for (const IdleBlock& b : v) {
+      cudaStreamWaitEvent(s, b.ev, 0);
+      cudaEventDestroy(b.ev);
+      cudaFreeAsync(b.p, s);
+    }
+  };
+  if (big) {
+    std::vector<IdleBlock> stale;
+    IdleBlock hit{nullptr, nullptr, 0};
+    {
+      std::lock_guard<std::mutex> lk(bc.m);
+      auto it = bc.idle.find(bytes);
+      if (it != bc.idle.end()) {
+        hit = it->second;
+        bc.idle.erase(it);
+        bc.live[hit.p] = bytes;
+      } else {
+        const uint64_t cur = g_gen.load();
+        for (auto i = bc.idle.begin(); i != bc.idle.end();)
+          if (i->second.gen + 2 <= cur) {
+            stale.push_back(i->second);
+            i = bc.idle.erase(i);
+          } else {
+            ++i;
+          }
+      }
+    }
+    if (hit.p) {
+      cudaError_t e = cudaStreamWaitEvent(s, hit.ev, 0);
+      cudaEventDestroy(hit.ev);
+      if (e != cudaSuccess) return e;
+      *p = hit.p;
+      return cudaSuccess;
+    }
+    if (dbg && !stale.empty())
+      std::fprintf(stderr, "[kc host] block cache: %zu stale blocks released\n", stale.size());
+    release(stale);
+  }
+  cudaMemPool_t pool = g_pools[dev & 63];
+  cudaError_t e = pool ? cudaMallocFromPoolAsync(p, bytes, pool, s) : cudaMallocAsync(p, bytes, s);
+  if (e == cudaErrorMemoryAllocation) {  // hand every idle block back and retry
+    cudaGetLastError();
+    std::vector<IdleBlock> all;
+    {
+      std::lock_guard<std::mutex> lk(bc.m);
+      for (auto& kv : bc.idle) all.push_back(kv.second);
+      bc.idle.clear();
+    }
+    release(all);
+    cudaStreamSynchronize(s);
+    e = pool ? cudaMallocFromPoolAsync(p, bytes, pool, s) : cudaMallocAsync(p, bytes, s);
+  }
+  if (e == cudaSuccess && big) {
+    std::lock_guard<std::mutex> lk(bc.m);
+    bc.live[*p] = bytes;
+  }
   if (dbg) {
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (ms > 0.5) std::fprintf(stderr, "[kc host] dmalloc %zu bytes: %.3f ms\n", bytes, ms);
@@ -66,7 +174,31 @@ cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t s) {
   return e;
 }
 void dfree(void* p, cudaStream_t s) {
-  if (p) cudaFreeAsync(p, s);
+  if (!p) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  BlockCache& bc = g_cache[dev & 63];
+  size_t bytes = 0;
+  {
+    std::lock_guard<std::mutex> lk(bc.m);
+    auto it = bc.live.find(p);
+    if (it != bc.live.end()) {
+      bytes = it->second;
+      bc.live.erase(it);
+    }
+  }
+  if (bytes) {  // a large block: keep it for the next request of this size
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess &&
+        cudaEventRecord(ev, s) == cudaSuccess) {
+      std::lock_guard<std::mutex> lk(bc.m);
+      bc.idle.emplace(bytes, IdleBlock{p, ev, g_gen.load()});
+      return;
+    }
+    if (ev) cudaEventDestroy(ev);
+    cudaGetLastError();
+  }
+  cudaFreeAsync(p, s);
 }
 }  // namespace kcb
 
@@ -521,6 +653,7 @@ kc_status upload_common(const kc_csr_view* csr, int device, bool on_device, uint
                         kc_graph** out) {
   kcb::DeviceGuard device_guard;  // restore the caller's current device
   HostClock hc;
+  kcb::blockcache::g_gen.fetch_add(1);  // (the block cache ages its idle blocks by uploads)
   if (!out) return fail(KC_ERR_INVALID_ARGUMENT, "out is null");
   *out = nullptr;
   if (!csr) return fail(KC_ERR_INVALID_ARGUMENT, "csr view is null");
@@ -785,6 +918,7 @@ void kc_graph_free(kc_graph* g) {
   if (g->stream) cudaStreamDestroy(g->stream);
   delete g;
   hc.mark("graph_free");
+  if (hc.on) kcb::pool_debug("after free");
 }
 
 uint32_t kc_graph_n(const kc_graph* g) { return g ? g->n : 0; }

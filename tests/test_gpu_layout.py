@@ -97,3 +97,19 @@ def test_layout_chunked_upload(gpu, oracle):
     a = H.layout()
     b = Hd.layout()
     assert all(np.array_equal(x, y) for x, y in zip(a[:3], b[:3])) and a[3] and b[3]
+
+
+def test_one_shot_alternating_sizes(gpu, oracle):
+    """kc_fastk_run recycles its large device blocks by exact size between
+    calls (kc_api.cu block cache) and releases the sizes of a graph it has not
+    seen for two uploads: alternate graphs of different sizes (blocks >= 1 MB)
+    and repeat one of them — every result must equal the oracle's peel."""
+    cases = []
+    for scale, ef, seed in ((17, 16, 1), (16, 24, 2), (18, 8, 3)):
+        g = oracle.build_csr(1 << scale, oracle.gen_rmat(scale, ef, seed))
+        cases.append((gpu.Graph(g.off, g.nbr), oracle.peel(g)))
+    order = [0, 1, 0, 2, 2, 1, 0, 0, 2, 1]
+    for i in order:
+        G, truth = cases[i]
+        core, st = gpu.fastk_run_abi(G)
+        assert np.array_equal(core, truth), i
