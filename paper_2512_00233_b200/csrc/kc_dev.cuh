@@ -386,7 +386,9 @@ __device__ __forceinline__ uint4 ld_ids4_rt(const uint32_t* p, bool ro) {
 
 // KC_STREAM_K: entries per thread per step (8: two 128-bit id loads, 4: one);
 // KC_STREAM_PREFETCH: the next step's ids are loaded before this step's
-// gathers are consumed (8 more live registers).  The per-phase kernels
+// gathers are consumed (8 more live registers); 2 (4-entry streams only): also
+// the next step's gathers are issued before this step is consumed (measured
+// 4% slower: profiles/r02/stream_pf2_ab.txt).  The per-phase kernels
 // (kc_count_split.cu) trade both for resident warps.  The callback always
 // sees 8 slots; with K = 4 the upper four are never valid (compile-time
 // zero bits of `ok`, so their code folds away).
@@ -410,6 +412,55 @@ __device__ __forceinline__ void stream_row_rt(const uint32_t* src, bool ro, cons
   const uint32_t len = (uint32_t)(oe - ob);
   const uint32_t end = head + len;            // relative end
   const uint32_t l0 = 4 * me, l1 = 4 * me + 4 * NT;
+#if KC_STREAM_PREFETCH == 2
+  if constexpr (K == 4) {
+    // Two-deep pipeline: the gathers of step a + 1 are issued before step a is
+    // consumed (and the ids of step a + 2 are loaded), so a step waits for
+    // max(gather, the consumer's own round trips) instead of their sum.
+    auto gather4 = [&](const uint4& q, uint32_t a, uint32_t (&xx)[4], uint32_t& okk, bool& pst) {
+      okk = 0;
+      pst = false;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t id = u4_get(q, k);
+        const bool in = a + l0 + k - head < len;
+        const bool v = in && id < cut;
+        pst |= in && !v;
+        okk |= (uint32_t)v << k;
+        xx[k] = v ? est_at(s_cache, cache_n, snap, id) : 0u;
+      }
+    };
+    uint4 qa = make_uint4(0, 0, 0, 0), qb = qa;
+    if (l0 < end) qa = ld_ids4_rt(base, ro);
+    if (STEP + l0 < end) qb = ld_ids4_rt(base + STEP, ro);
+    uint32_t xa[4], oka;
+    bool pasta;
+    gather4(qa, 0, xa, oka, pasta);
+    for (uint32_t a = 0; a < end; a += STEP) {
+      const uint32_t nb = a + STEP;
+      uint32_t xb[4] = {0, 0, 0, 0}, okb = 0;
+      bool pastb = false;
+      if (nb < end) gather4(qb, nb, xb, okb, pastb);
+      uint4 qc = make_uint4(0, 0, 0, 0);
+      if (nb + STEP + l0 < end) qc = ld_ids4_rt(base + nb + STEP, ro);
+      uint32_t ids[8], x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        ids[k] = k < 4 ? u4_get(qa, k & 3) : 0u;
+        x[k] = k < 4 ? xa[k & 3] : 0u;
+      }
+      f(oka, ids, x);
+      if (stop && __any_sync(FULL, pasta)) break;
+      qa = qb;
+      qb = qc;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) xa[k] = xb[k];
+      oka = okb;
+      pasta = pastb;
+    }
+    return;
+  }
+#endif
   uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
   if (PF) {
     if (l0 < end) q0 = ld_ids4_rt(base, ro);
