@@ -2079,12 +2079,15 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
   // functions read it through a reference (a stack copy would be local
   // memory, which misses L1 under this kernel's stack footprint)
   __shared__ View<EstT> s_view;
+  __shared__ __align__(8) unsigned long long s_mbar;  // the cache fills' TMA barrier
+  uint32_t fill_phase = 0;
   const View<EstT>& v = s_view;
   uint32_t* wn = s_wn[warp_id()];
   const uint32_t tid = threadIdx.x;
   Enq q;
   q.wbuf = s_wq + (size_t)warp_id() * NCLS * WQ;
   q.wn = wn;
+  if (tid == 0) mbar_init(&s_mbar);
   if (tid == 0) sh.ticket = 0xffffffffu;
   if (lane_id() < NCLS) wn[lane_id()] = 0;
   if (tid < DEG_SUB_MAX + 2) s_dcut[tid] = p.dc.at(tid);
@@ -2141,7 +2144,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     const uint32_t cache_n = active >= CACHE_MIN_ACTIVE ? p.cache_n : 0u;
     vl.cache_n = cache_n;
     if (r > 0 && active < WML_SMALL_ACTIVE) vl.wml = WML_SMALL;
-    if (cache_n && !evaluated) fill_cache(s_cache, (const EstT*)p.E, cache_n);
+    if (cache_n && !evaluated) fill_cache_bulk(smem, s_cache, (const EstT*)p.E, cache_n, &s_mbar, fill_phase);
     if (tid == 0) s_view = vl;
     __syncthreads();
     Acc acc{0, 0, 0, 0, 0, 0, false};
@@ -2191,7 +2194,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
       vl.grab = p.ctl[cur].grab2;
       vl.r0 = false;
       vl.pull = true;
-      if (cache_n) fill_cache(s_cache, (const EstT*)p.N, cache_n);
+      if (cache_n) fill_cache_bulk(smem, s_cache, (const EstT*)p.N, cache_n, &s_mbar, fill_phase);
       if (tid == 0) s_view = vl;
       __syncthreads();
       if (pf) pf[6] = gtimer();
@@ -2211,7 +2214,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1) count_rounds_kernel(const __
     // ---------------- NOTIFY + APPLY ----------------
     vl.snap = p.N;
     vl.grab = p.ctl[cur].grab2;
-    if (cache_n) fill_cache(s_cache, (const EstT*)p.N, cache_n);
+    if (cache_n) fill_cache_bulk(smem, s_cache, (const EstT*)p.N, cache_n, &s_mbar, fill_phase);
     if (tid == 0) s_view = vl;
     __syncthreads();
     if (pf) pf[6] = gtimer();
@@ -2262,11 +2265,14 @@ __global__ void __launch_bounds__(SOLVE_THREADS, KC_SPLIT_CTAS)
   __shared__ Shared sh;
   __shared__ uint32_t s_qcnt[NCLS];
   __shared__ View<EstT> s_view;
+  __shared__ __align__(8) unsigned long long s_mbar;  // the cache fill's TMA barrier
+  uint32_t fill_phase = 0;
   const View<EstT>& v = s_view;
   uint32_t* wn = s_wn[warp_id()];
   const uint32_t tid = threadIdx.x;
   const uint32_t cur = r & 1, nxt = cur ^ 1;
   const uint32_t sr = r < STAT_SLOTS - 1 ? r : STAT_SLOTS - 1;
+  if (tid == 0) mbar_init(&s_mbar);
   if (tid == 0) sh.ticket = 0xffffffffu;
   if (lane_id() < NCLS) wn[lane_id()] = 0;
   if (tid < NCLS) s_qcnt[tid] = p.ctl[cur].qcnt[tid];
@@ -2311,7 +2317,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, KC_SPLIT_CTAS)
     if (skip_eval) return;  // round 1 after PULL: evaluated already
     vl.snap = p.E;
     vl.grab = p.ctl[cur].grab;
-    if (cache_n) fill_cache(s_cache, (const EstT*)p.E, cache_n);
+    if (cache_n) fill_cache_bulk(smem, s_cache, (const EstT*)p.E, cache_n, &s_mbar, fill_phase);
     if (tid == 0) s_view = vl;
     __syncthreads();
     if (pf) pf[1] = gtimer();
@@ -2331,7 +2337,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, KC_SPLIT_CTAS)
     }
     vl.snap = p.N;
     vl.grab = p.ctl[cur].grab2;
-    if (cache_n) fill_cache(s_cache, (const EstT*)p.N, cache_n);
+    if (cache_n) fill_cache_bulk(smem, s_cache, (const EstT*)p.N, cache_n, &s_mbar, fill_phase);
     if (tid == 0) s_view = vl;
     __syncthreads();
     if (pf) pf[6] = gtimer();

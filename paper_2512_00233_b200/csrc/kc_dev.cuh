@@ -586,5 +586,54 @@ __device__ __forceinline__ void fill_cache(EstT* s_cache, const EstT* src, uint3
   }
 }
 
+// The same fill as one TMA bulk copy (cp.async.bulk global -> shared,
+// completion on an mbarrier; UBLKCP in SASS): one thread issues it, every
+// thread waits on the barrier's phase.  No registers, no LSU instructions and
+// no shared-memory stores per thread.  `smem_cache` is the 16-byte aligned
+// start of the cache, cache_n * sizeof(EstT) a multiple of 16 bytes.  The
+// previous readers of the cache are behind a CTA or grid barrier (every call
+// site); the proxy fence orders their generic-proxy reads before the async
+// proxy's writes.
+#ifndef KC_TMA_FILL
+#define KC_TMA_FILL 1
+#endif
+__device__ __forceinline__ void mbar_init(unsigned long long* mbar) {  // one thread, before a CTA barrier
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(mbar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+template <typename EstT>
+__device__ __forceinline__ void fill_cache_bulk(void* smem_cache, EstT* s_cache, const EstT* src,
+                                                uint32_t cache_n, unsigned long long* mbar,
+                                                uint32_t& phase) {
+#if KC_TMA_FILL
+  (void)s_cache;
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = (uint32_t)((size_t)cache_n * sizeof(EstT));
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(smem_cache);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(mb)
+        : "memory");
+  }
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(mb), "r"(phase)
+        : "memory");
+  } while (!done);
+  phase ^= 1u;
+#else
+  (void)smem_cache;
+  (void)mbar;
+  (void)phase;
+  fill_cache(s_cache, src, cache_n);
+#endif
+}
+
 }  // namespace dev
 }  // namespace kcb
