@@ -206,6 +206,12 @@ kc_status kc_sequential_tail(kc_graph* g, uint32_t* est, uint8_t* active, int ex
 kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* coreness,
                        kc_stats* stats);
 
+/* The library keeps the device memory of freed handles and finished one-shot
+ * solves for the next call (its own stream-ordered pool, plus large blocks
+ * recycled by exact size).  kc_trim_memory hands all of it back to the
+ * driver (current device); live handles are not touched. */
+kc_status kc_trim_memory(void);
+
 /* The CUDA stream a handle runs on (cudaStream_t as void*), for callers that
  * want to time kc_solve_device with their own events. */
 void* kc_graph_stream(kc_graph* g);

@@ -41,4 +41,5 @@ from .api import (  # noqa: F401
     make_coreness_result,
     should_notify,
     switch_condition,
+    trim_memory,
 )

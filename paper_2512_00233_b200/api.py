@@ -71,7 +71,7 @@ ABI_SYMBOLS = (
     "kc_csr_dev_free", "kc_csr_dev_download", "kc_debug_phase_times", "kc_graph_upload_ex",
     "kc_debug_round_stats", "kc_debug_gather_probe", "kc_solve_traced", "kc_peel", "kc_verify", "kc_load_edge_list",
     "kc_load_edge_list_file", "kc_csr_dev_original_ids", "kc_sequential_tail",
-    "kc_debug_layout",
+    "kc_debug_layout", "kc_trim_memory",
 )
 KC_DEBUG_PHASE_TIMES = 1
 KC_DEBUG_LEGACY_COUNT = 2
@@ -159,6 +159,8 @@ def load_library():
     L.kc_debug_round_stats.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32]
     L.kc_debug_gather_probe.restype = C.c_int
     L.kc_debug_gather_probe.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_float)]
+    L.kc_trim_memory.restype = C.c_int
+    L.kc_trim_memory.argtypes = []
     L.kc_debug_layout.restype = C.c_int
     L.kc_debug_layout.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                   C.POINTER(C.c_uint32), C.POINTER(C.c_int)]
@@ -425,6 +427,11 @@ def load_edge_list_file(path: str, device: int = 0) -> DeviceCSR:
         raise IoError(err.what.decode(errors="replace"))
     _check(st, "kc_load_edge_list_file")
     return DeviceCSR(p)
+
+
+def trim_memory() -> None:
+    """Hand the device memory the library keeps between calls back to the driver."""
+    _check(load_library().kc_trim_memory(), "kc_trim_memory")
 
 
 def gen_config(cfg: int, p0: int, p1: int = 0, p2: int = 0, seed: int = 1,

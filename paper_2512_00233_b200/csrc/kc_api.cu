@@ -173,6 +173,26 @@ cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t s) {
   }
   return e;
 }
+cudaError_t trim_memory() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  BlockCache& bc = g_cache[dev & 63];
+  std::vector<IdleBlock> all;
+  {
+    std::lock_guard<std::mutex> lk(bc.m);
+    for (auto& kv : bc.idle) all.push_back(kv.second);
+    bc.idle.clear();
+  }
+  for (const IdleBlock& b : all) {
+    cudaEventSynchronize(b.ev);
+    cudaEventDestroy(b.ev);
+    cudaFreeAsync(b.p, nullptr);
+  }
+  if ((e = cudaStreamSynchronize(nullptr)) != cudaSuccess) return e;
+  if (g_pools[dev & 63]) return cudaMemPoolTrimTo(g_pools[dev & 63], 0);
+  return cudaSuccess;
+}
 void dfree(void* p, cudaStream_t s) {
   if (!p) return;
   int dev = 0;
@@ -923,6 +943,19 @@ void kc_graph_free(kc_graph* g) {
 
 uint32_t kc_graph_n(const kc_graph* g) { return g ? g->n : 0; }
 uint64_t kc_graph_nnz(const kc_graph* g) { return g ? g->nnz : 0; }
+kc_status kc_trim_memory(void) {
+  g_last_error.clear();
+  int cur = 0, sms = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(KC_ERR_NO_DEVICE, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  kc_status s = check_device(cur, &sms);
+  if (s != KC_OK) return s;
+  CK(kcb::trim_memory());
+  return KC_OK;
+}
+
 void* kc_graph_stream(kc_graph* g) { return g ? (void*)g->stream : nullptr; }
 
 kc_status kc_graph_timings(const kc_graph* g, float* tu, float* tp) {
