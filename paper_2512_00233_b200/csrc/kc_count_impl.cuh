@@ -164,6 +164,9 @@ constexpr int WQ = KC_WQ;          // per-warp, per-class enqueue buffer (flushe
 #ifndef KC_R0_SORTED
 #define KC_R0_SORTED 1             // round 0 on sorted rows without gathers (r0_sorted_warp)
 #endif
+#ifndef KC_R0_LANE
+#define KC_R0_LANE 1               // ... BIG / WARP rows by a lane each, binary searches (r0_sorted_lane)
+#endif
 #ifndef KC_LIST_SHIFT
 #define KC_LIST_SHIFT 1            // list threshold L = t - (t >> KC_LIST_SHIFT)
 #endif
@@ -866,6 +869,20 @@ __device__ void consume_long(const CP<OffT, EstT>& p, const View<EstT>& v, Share
 template <bool PULL, typename OffT, typename EstT, typename A>
 __device__ __forceinline__ void eval_wclass_impl(const CP<OffT, EstT>& p, const View<EstT>& v, const EstT* s_cache,
                             uint32_t* bins, int c, uint32_t gmax, A& acc) {
+#if KC_R0_LANE
+  if (KC_R0_SORTED && !PULL && v.r0 && p.dc.sorted) {
+    // round 0 on sorted rows: a lane per vertex, two binary searches (r0_sorted_lane)
+    for_class(p, v, c, 32u, [&](uint32_t u, uint32_t n) {
+      if (lane_id() < n) {
+        const Item it = eval_item<PULL>(p, v, s_cache, u);
+        uint32_t probes = 0;
+        const uint2 tc = r0_sorted_lane(p.adj, p.dc.t, it.ob, it.deg, it.cap, probes);
+        finish_eval<PULL>(p, v, it, tc.x, tc.y, probes, acc);
+      }
+    });
+    return;
+  }
+#endif
   for_class(p, v, c, gmax, [&](uint32_t u, uint32_t n) {
     Item mine{};
     if (lane_id() < n) {

@@ -564,6 +564,36 @@ __device__ __forceinline__ uint2 r0_sorted_warp(const uint32_t* adj, const uint3
   return make_uint2(t, t + __reduce_add_sync(FULL, c));
 }
 
+// The same rule by one lane: both quantities are monotone along a sorted row
+// (row ids ascend, the cut table descends), so t is the last position i <= cap
+// with row[i-1] < cut(i) and count(E >= t) the first position j >= t with
+// row[j] >= cut(t) — two binary searches, ~2 log2(deg) probes of one sector
+// each instead of streaming the row (count(E >= t) is nearly the whole row for
+// most vertices).  A warp evaluates 32 vertices at once.  `probes`: entries
+// read.
+__device__ __forceinline__ uint2 r0_sorted_lane(const uint32_t* adj, const uint32_t* dcut,
+                                                uint64_t ob, uint32_t deg, uint32_t cap,
+                                                uint32_t& probes) {
+  const uint32_t* row = adj + ob;
+  uint32_t lo = 0, hi = cap < deg ? cap : deg, np = 0;
+  while (lo < hi) {  // largest i with row[i-1] < cut(i) (holds on a prefix; i = 0: vacuous)
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    const uint32_t id = __ldg(row + mid - 1), ct = __ldg(dcut + mid);
+    ++np;
+    if (id < ct) lo = mid; else hi = mid - 1;
+  }
+  const uint32_t t = lo;
+  const uint32_t ctt = __ldg(dcut + t);
+  hi = deg;
+  while (lo < hi) {  // first j >= t with row[j] >= cut(t)
+    const uint32_t mid = (lo + hi) >> 1;
+    ++np;
+    if (__ldg(row + mid) < ctt) lo = mid + 1; else hi = mid;
+  }
+  probes = np;
+  return make_uint2(t, lo);
+}
+
 template <typename EstT>
 __device__ __forceinline__ void fill_cache(EstT* s_cache, const EstT* src, uint32_t cache_n) {
   // cache_n * sizeof(EstT) is a multiple of 16 bytes; 8 loads in flight per
