@@ -50,6 +50,10 @@ namespace cg = cooperative_groups;
 constexpr uint32_t HUB_FINE = 256;
 #ifndef KC_SOLVE_R0
 #define KC_SOLVE_R0 1    // round 0 on sorted rows by the prefix rule (r0_sorted_warp)
+#ifndef KC_SOLVE_R0_LANE
+#define KC_SOLVE_R0_LANE 0  // ... BIG / WARP rows by a lane each (r0_sorted_lane): slower here (8-16
+                            // items per grab leave most lanes idle: R-MAT 26 137 -> 143 ms)
+#endif
 #endif
 
 namespace kcb {
@@ -440,6 +444,15 @@ __device__ void eval_wstream(const P<OffT, EstT>& p, const RoundView<EstT>& rv,
   for_queue<G>(p.queue + p.cb[cls], rv.qcnt[cls], &rv.grab[cls],
                [&](const uint32_t* lst, uint32_t n) {
     const Meta mine = load_meta(p, rv.snap, s_cache, rv.cache_n, lst, n);
+    if (KC_SOLVE_R0 && KC_SOLVE_R0_LANE && rv.r0 && p.sorted) {
+      // round 0 on sorted rows: a lane per vertex, two binary searches (r0_sorted_lane, kc_dev.cuh)
+      if (lane < n) {
+        uint32_t sc = 0;
+        const uint2 tc = r0_sorted_lane(p.adj, p.dcut, mine.ob, (uint32_t)(mine.oe - mine.ob), mine.cap, sc);
+        finish_eval(p, rv, mine.u, tc.x, mine.cap, tc.y, mine.oe - mine.ob, acc);
+      }
+      return;
+    }
     for (uint32_t i = 0; i < n; ++i) {
       const Meta it = shfl_meta(mine, i);
       const uint32_t cap = it.cap;
