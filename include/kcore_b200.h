@@ -212,6 +212,11 @@ kc_status kc_fastk_run(const kc_csr_view* csr, const kc_options* opt, uint32_t* 
  * driver (current device); live handles are not touched. */
 kc_status kc_trim_memory(void);
 
+/* Debug: the host-side copy of the pageable staging path (non-temporal AVX2
+ * stores where the CPU has them, memcpy otherwise); needs no device.  For
+ * tests. */
+void kc_debug_host_copy(void* dst, const void* src, uint64_t bytes);
+
 /* The CUDA stream a handle runs on (cudaStream_t as void*), for callers that
  * want to time kc_solve_device with their own events. */
 void* kc_graph_stream(kc_graph* g);

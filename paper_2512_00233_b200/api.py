@@ -71,7 +71,7 @@ ABI_SYMBOLS = (
     "kc_csr_dev_free", "kc_csr_dev_download", "kc_debug_phase_times", "kc_graph_upload_ex",
     "kc_debug_round_stats", "kc_debug_gather_probe", "kc_solve_traced", "kc_peel", "kc_verify", "kc_load_edge_list",
     "kc_load_edge_list_file", "kc_csr_dev_original_ids", "kc_sequential_tail",
-    "kc_debug_layout", "kc_trim_memory",
+    "kc_debug_layout", "kc_trim_memory", "kc_debug_host_copy",
 )
 KC_DEBUG_PHASE_TIMES = 1
 KC_DEBUG_LEGACY_COUNT = 2
@@ -159,6 +159,8 @@ def load_library():
     L.kc_debug_round_stats.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32]
     L.kc_debug_gather_probe.restype = C.c_int
     L.kc_debug_gather_probe.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_float)]
+    L.kc_debug_host_copy.restype = None
+    L.kc_debug_host_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64]
     L.kc_trim_memory.restype = C.c_int
     L.kc_trim_memory.argtypes = []
     L.kc_debug_layout.restype = C.c_int

@@ -956,6 +956,10 @@ kc_status kc_trim_memory(void) {
   return KC_OK;
 }
 
+void kc_debug_host_copy(void* dst, const void* src, uint64_t bytes) {
+  kcb::host_copy(dst, src, (size_t)bytes);
+}
+
 void* kc_graph_stream(kc_graph* g) { return g ? (void*)g->stream : nullptr; }
 
 kc_status kc_graph_timings(const kc_graph* g, float* tu, float* tp) {

@@ -66,3 +66,22 @@ def test_graph_rejects_malformed_csr():
         K.Graph(np.array([0, 1, 2], np.uint64), np.array([1, 5], np.uint32))  # id >= n
     with pytest.raises(ValueError):
         K.Graph(np.array([1, 2], np.uint64), np.array([0], np.uint32))  # offsets[0] != 0
+
+
+def test_host_copy_every_alignment(kc):
+    """kc_hostcopy.cpp (the pageable staging path's host copy: non-temporal
+    stores behind a run-time AVX2 check, memcpy otherwise): byte-exact for
+    every destination / source misalignment and for sizes around the 64 KB
+    switch and the 128-byte inner step; bytes outside the range untouched."""
+    import numpy as np
+    L = kc.load_library()
+    rng = np.random.default_rng(7)
+    src = rng.integers(0, 256, 1 << 20, dtype=np.uint8)
+    sizes = [0, 1, 31, 32, 33, 127, 128, 129, 4095, 65535, 65536, 65537, 65536 + 127, 200001, 524288 + 77]
+    for n in sizes:
+        for da in (0, 1, 7, 31, 33):
+            for sa in (0, 3, 32, 63):
+                dst = np.full(n + 256, 0xA5, dtype=np.uint8)
+                L.kc_debug_host_copy(dst.ctypes.data + 64 + da, src.ctypes.data + sa, n)
+                assert np.array_equal(dst[64 + da: 64 + da + n], src[sa: sa + n]), (n, da, sa)
+                assert np.all(dst[: 64 + da] == 0xA5) and np.all(dst[64 + da + n:] == 0xA5), (n, da, sa)
