@@ -359,7 +359,11 @@ def run_ours(args, ws, rank, local):
             if c == args.config:
                 continue
             torch.cuda.empty_cache()
-            a = measure(K, torch, c, args, local, 5, 3, 3)
+            try:
+                a = measure(K, torch, c, args, local, 5, 3, 3)
+            except Exception as e:  # reported, never fatal to the headline line
+                also[f"cfg{c}"] = {"error": f"{type(e).__name__}: {e}"}
+                continue
             a.pop("host")
             sta = a["st"]
             also[f"cfg{c}"] = {
